@@ -1,0 +1,139 @@
+/*
+ * pasgal_bcc.h -- C-ABI of the B200-native FAST-BCC library (libpasgal_bcc.so).
+ *
+ * Drop-in boundary for the reference's biconnectivity entry point
+ *   pasgal.oracles.bcc_hopcroft_tarjan(g) -> BccLabels
+ *     (/root/reference/pkg/src/pasgal/oracles.py:119-201; output type results.py:45-88)
+ * and for the absent parallel `bcc` module it specifies.
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures.  Every
+ * pointer named "device" is a CUDA device pointer; `stream` is a cudaStream_t passed
+ * as void* (NULL = legacy default stream).  All work is stream-ordered and
+ * asynchronous unless a function says it synchronises.  The library never allocates
+ * device memory: the caller owns inputs, outputs and the workspace.
+ *
+ * Status codes (mapped by the Python wrapper to the reference's exceptions):
+ *   0 PASGAL_OK
+ *   1 PASGAL_EINVAL      bad argument           -> ValueError
+ *   2 PASGAL_ENOTSYM     not symmetric/simple   -> ValueError("biconnectivity requires a
+ *                        symmetric graph")  (oracles.py:127-128)
+ *   3 PASGAL_EWORKSPACE  workspace too small    -> ValueError
+ *   4 PASGAL_ECUDA       CUDA runtime error     -> RuntimeError
+ *   5 PASGAL_EUNSORTED   rows not sorted        -> ValueError
+ *   6 PASGAL_ERANGE      target out of range / bad offsets (graph.py:87-96) -> ValueError
+ */
+#ifndef PASGAL_BCC_H
+#define PASGAL_BCC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PASGAL_OK 0
+#define PASGAL_EINVAL 1
+#define PASGAL_ENOTSYM 2
+#define PASGAL_EWORKSPACE 3
+#define PASGAL_ECUDA 4
+#define PASGAL_EUNSORTED 5
+#define PASGAL_ERANGE 6
+
+/* flags for pasgal_bcc */
+#define PASGAL_BCC_CANONICAL 1u   /* edge_label = min undirected edge id of the BCC */
+
+/* Symmetric CSR on the device.  Replaces the reference's Graph (graph.py:54-77):
+ * offsets int64[n+1] (offsets[n] == m_slots), targets int32[m_slots].
+ * Limits: n < 2^31, m_slots < 2^32. */
+typedef struct {
+    int64_t n;
+    int64_t m_slots;
+    const int64_t* offsets;   /* device */
+    const int32_t* targets;   /* device */
+} pasgal_csr_t;
+
+/* Outputs (device).  Replaces BccLabels (results.py:45-66):
+ *   edge_label  uint32[m_slots]  one id per BCC, equal on both directions of an edge
+ *               (raw: a skeleton component id; CANONICAL: the rank of the BCC's smallest
+ *               u<v slot among all u<v slots in CSR order).  Slots of isolated vertices:
+ *               none exist.
+ *   artic_bits  uint32[ceil(n/32)] articulation bitmap, bit v&31 of word v>>5.
+ *   bcc_count   int64 scalar (device).
+ *   comp/parent/first  optional uint32[n] (NULL to skip): the parallel-mode fields of
+ *               BccLabels (results.py:76-88): skeleton component, spanning-forest parent
+ *               (self for roots), preorder rank. */
+typedef struct {
+    uint32_t* edge_label;
+    uint32_t* artic_bits;
+    int64_t* bcc_count;
+    uint32_t* comp;
+    uint32_t* parent;
+    uint32_t* first;
+} pasgal_bcc_out_t;
+
+/* Workspace for pasgal_bcc / pasgal_csr_validate: O(n) plus O((n+m)/2048) tile
+ * partition entries ("O(n) auxiliary space"). */
+size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots);
+
+/* FAST-BCC on a symmetric, simple CSR with sorted rows.  Asynchronous.  Input is not
+ * validated here beyond argument checks; see pasgal_csr_validate.  `seed` perturbs
+ * sampling only; canonical outputs are seed-invariant. */
+int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace,
+               size_t workspace_bytes, uint64_t seed, uint32_t flags, void* stream);
+
+/* Device validation of the BCC preconditions (graph.py:87-96, 123-158):
+ * offsets monotone from 0 to m_slots, targets in [0,n), rows strictly increasing (sorted,
+ * no duplicates), no self-loops, and every slot u->w has its reverse w->u.
+ * SYNCHRONISES `stream`; returns the status (PASGAL_OK, _ERANGE, _EUNSORTED, _ENOTSYM). */
+int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* ---------------- device graph construction (north-star subsystem 1) ---------------- */
+
+/* Temp bytes for pasgal_csr_from_keys with `nkeys` keys on n vertices. */
+size_t pasgal_csr_build_temp_bytes(int64_t n, int64_t nkeys);
+
+/* Directed edge keys (u<<32 | w) -> sorted, deduplicated CSR with self-loops dropped
+ * (the contract of symmetrize/from_edges, graph.py:176-194, 452-481; the keys must
+ * already contain both directions).  keys[] and keys_alt[] (both uint64[nkeys]) are
+ * clobbered.  offsets int64[n+1]; targets int32 with room for nkeys entries.  Writes the
+ * slot count to *m_slots_dev.  Asynchronous. */
+int pasgal_csr_from_keys(int64_t n, uint64_t* keys, uint64_t* keys_alt, int64_t nkeys,
+                         int64_t* offsets, int32_t* targets, int64_t* m_slots_dev,
+                         void* temp, size_t temp_bytes, void* stream);
+
+/* Generators (rules pinned in DESIGN.md "Generators"; host twins in oracle/gen_host.c).
+ * draw(seed, c) = sm64(sm64(seed) ^ c), sm64 = the splitmix64 finaliser. */
+
+/* rows x cols 4-neighbour lattice, candidate edge e kept iff draw(seed,e) < keep_threshold
+ * (or always when keep_all).  Writes the sorted symmetric CSR directly: offsets int64[n+1],
+ * targets int32 (capacity 4*rows*cols), *m_slots_dev.  `temp` >= pasgal_gen_grid_temp_bytes. */
+size_t pasgal_gen_grid_temp_bytes(int64_t rows, int64_t cols);
+int pasgal_gen_grid(int64_t rows, int64_t cols, uint64_t seed, uint64_t keep_threshold,
+                    int keep_all, int64_t* offsets, int32_t* targets, int64_t* m_slots_dev,
+                    void* temp, size_t temp_bytes, void* stream);
+
+/* RMAT: `draws` edges on 2^scale vertices; quadrant thresholds ta <= tab <= tabc on 32-bit
+ * uniforms.  Emits both directions of every non-loop draw into keys (capacity 2*draws);
+ * *nkeys_dev receives the count. */
+int pasgal_gen_rmat_keys(int scale, int64_t draws, uint64_t seed, uint32_t ta, uint32_t tab,
+                         uint32_t tabc, uint64_t* keys, int64_t* nkeys_dev, void* stream);
+
+/* kNN: npts seeded points with 24-bit coordinates, k nearest (exact integer distance,
+ * ties by index, self excluded) on a 2^gbits x 2^gbits cell grid.  Emits both directions
+ * of every (i, neighbour) pair into keys (capacity 2*k*npts); *nkeys_dev = 2*k*npts'
+ * where npts' accounts for npts <= k.  `temp` >= pasgal_gen_knn_temp_bytes. */
+size_t pasgal_gen_knn_temp_bytes(int64_t npts, int gbits);
+int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t* keys,
+                        int64_t* nkeys_dev, void* temp, size_t temp_bytes, void* stream);
+
+/* Human-readable status text. */
+const char* pasgal_strerror(int status);
+
+/* Library version string. */
+const char* pasgal_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASGAL_BCC_H */

@@ -1,0 +1,20 @@
+"""paper_2404_17101_b200 -- B200-native FAST-BCC (PASGAL, arXiv 2404.17101).
+
+Drop-in for the reference package's biconnectivity entry point
+(pasgal.oracles.bcc_hopcroft_tarjan, oracles.py:119-201) built from hand-written sm_100a
+CUDA kernels behind a C-ABI (include/pasgal_bcc.h).  See DESIGN.md.
+"""
+
+from .results import BccLabels, canonical_edge_partition, canonical_relabel, min_eid_to_partition
+from .graph import (CONFIGS, DeviceGraph, Graph, csr_from_keys, gen_grid, gen_knn, gen_rmat, make_config,
+                    symmetrize_edges)
+from .bcc import DeviceBcc, bcc, bcc_device, release_workspace, unpack_articulation, validate_device, workspace_bytes
+
+__all__ = [
+    "BccLabels", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
+    "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",
+    "symmetrize_edges", "DeviceBcc", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
+    "validate_device", "workspace_bytes",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,95 @@
+"""ctypes binding of libpasgal_bcc.so (the C-ABI in include/pasgal_bcc.h).
+
+There is no fallback: if the library is missing or fails to load, every entry point
+raises.  ``load()`` never compiles on its own; ``build()`` (``__graft_entry__.build``)
+does that ahead of time so the .so travels with the repository.
+"""
+
+import ctypes
+import os
+
+from . import _build
+
+LIB_PATH = _build.LIB
+
+PASGAL_OK = 0
+PASGAL_EINVAL = 1
+PASGAL_ENOTSYM = 2
+PASGAL_EWORKSPACE = 3
+PASGAL_ECUDA = 4
+PASGAL_EUNSORTED = 5
+PASGAL_ERANGE = 6
+PASGAL_BCC_CANONICAL = 1
+
+
+class PasgalCsr(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m_slots", ctypes.c_int64),
+                ("offsets", ctypes.c_void_p), ("targets", ctypes.c_void_p)]
+
+
+class PasgalBccOut(ctypes.Structure):
+    _fields_ = [("edge_label", ctypes.c_void_p), ("artic_bits", ctypes.c_void_p),
+                ("bcc_count", ctypes.c_void_p), ("comp", ctypes.c_void_p),
+                ("parent", ctypes.c_void_p), ("first", ctypes.c_void_p)]
+
+
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_U32 = ctypes.c_uint32
+_INT = ctypes.c_int
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); must match include/pasgal_bcc.h exactly
+SIGNATURES = {
+    "pasgal_bcc_workspace_bytes": (_SZ, [_I64, _I64]),
+    "pasgal_bcc": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP]),
+    "pasgal_csr_validate": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
+    "pasgal_csr_build_temp_bytes": (_SZ, [_I64, _I64]),
+    "pasgal_csr_from_keys": (_INT, [_I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "pasgal_gen_grid_temp_bytes": (_SZ, [_I64, _I64]),
+    "pasgal_gen_grid": (_INT, [_I64, _I64, _U64, _U64, _INT, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "pasgal_gen_rmat_keys": (_INT, [_INT, _I64, _U64, _U32, _U32, _U32, _VP, _VP, _VP]),
+    "pasgal_gen_knn_temp_bytes": (_SZ, [_I64, _INT]),
+    "pasgal_gen_knn_keys": (_INT, [_I64, _INT, _U64, _INT, _VP, _VP, _VP, _SZ, _VP]),
+    "pasgal_strerror": (ctypes.c_char_p, [_INT]),
+    "pasgal_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+class PasgalError(RuntimeError):
+    pass
+
+
+def load():
+    """Load the in-tree shared library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libpasgal_bcc.so not found at {LIB_PATH}: build it first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def strerror(status):
+    return load().pasgal_strerror(status).decode()
+
+
+def check(status, what="pasgal"):
+    """Map a status code to the reference's exception types."""
+    if status == PASGAL_OK:
+        return
+    msg = strerror(status)
+    if status == PASGAL_ECUDA:
+        raise PasgalError(f"{what}: {msg}")
+    raise ValueError(msg if status == PASGAL_ENOTSYM else f"{what}: {msg}")

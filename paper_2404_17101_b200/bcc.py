@@ -1,0 +1,168 @@
+"""FAST-BCC entry points: the drop-in for the reference's BCC call.
+
+``bcc(g)`` has the call shape of ``pasgal.oracles.bcc_hopcroft_tarjan(g)``
+(oracles.py:119-201) and returns a ``BccLabels`` (results.py:45-88) that the reference's
+``canonical_edge_partition`` (results.py:103-112) accepts unchanged.  The work runs on the
+B200 through libpasgal_bcc.so (include/pasgal_bcc.h); there is no CPU fallback.
+
+``bcc_device(offsets, targets)`` is the device-resident form: torch CUDA tensors in,
+torch CUDA tensors out, stream-ordered on the current stream, no host synchronisation
+unless ``validate=True``.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import DeviceGraph
+from .results import BccLabels
+
+_ws_cache = {}
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def workspace_bytes(n, m):
+    return int(_lib.load().pasgal_bcc_workspace_bytes(int(n), int(m)))
+
+
+def _workspace(device, nbytes):
+    """A cached device workspace of at least nbytes (the library never allocates)."""
+    key = torch.device(device)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=key)
+        _ws_cache[key] = ws
+    return ws
+
+
+def release_workspace():
+    _ws_cache.clear()
+
+
+@dataclass
+class DeviceBcc:
+    """Device outputs of one BCC run."""
+
+    edge_label: torch.Tensor    # int32 storage of uint32 labels [M] (0xFFFFFFFF = none)
+    artic_bits: torch.Tensor    # int32 storage of the uint32 bitmap [ceil(n/32)]
+    bcc_count: torch.Tensor     # int64 [1]
+    comp: torch.Tensor = None   # optional int32 [n]
+    parent: torch.Tensor = None
+    first: torch.Tensor = None
+
+
+def _csr_struct(offsets, targets):
+    n = offsets.shape[0] - 1
+    m = targets.shape[0]
+    return _lib.PasgalCsr(n, m, offsets.data_ptr(), targets.data_ptr() if m else 0)
+
+
+def validate_device(offsets, targets, workspace=None):
+    """Device check of the BCC preconditions (symmetric, sorted rows, ids in range).
+    Synchronises; raises ValueError like the reference (oracles.py:127-128)."""
+    lib = _lib.load()
+    n, m = offsets.shape[0] - 1, targets.shape[0]
+    need = workspace_bytes(n, m)
+    ws = workspace if workspace is not None else _workspace(offsets.device, need)
+    csr = _csr_struct(offsets, targets)
+    st = lib.pasgal_csr_validate(ctypes.byref(csr), _vp(ws), ws.numel(),
+                                 ctypes.c_void_p(torch.cuda.current_stream(offsets.device).cuda_stream))
+    _lib.check(st, "validate")
+
+
+def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out=None,
+               workspace=None, forest=False):
+    """FAST-BCC on a device CSR (offsets int64[n+1], targets int32[M], both CUDA).
+
+    Returns ``DeviceBcc``.  ``canonical=True`` labels every edge with the minimum
+    undirected edge id of its BCC.  ``forest=True`` also returns comp/parent/first (the
+    parallel-mode fields of BccLabels)."""
+    lib = _lib.load()
+    if offsets.device.type != "cuda" or targets.device.type != "cuda":
+        raise ValueError("bcc_device needs CUDA tensors")
+    if offsets.dtype != torch.int64 or targets.dtype != torch.int32:
+        raise ValueError("offsets must be int64 and targets int32")
+    offsets = offsets.contiguous()
+    targets = targets.contiguous()
+    n, m = offsets.shape[0] - 1, targets.shape[0]
+    dev = offsets.device
+    need = workspace_bytes(n, m)
+    ws = workspace if workspace is not None else _workspace(dev, need)
+    if ws.numel() < need:
+        raise ValueError("workspace too small")
+    if validate:
+        validate_device(offsets, targets, ws)
+    if out is None:
+        out = DeviceBcc(
+            edge_label=torch.empty(m, dtype=torch.int32, device=dev),
+            artic_bits=torch.empty((n + 31) // 32, dtype=torch.int32, device=dev),
+            bcc_count=torch.empty(1, dtype=torch.int64, device=dev),
+        )
+        if forest:
+            out.comp = torch.empty(n, dtype=torch.int32, device=dev)
+            out.parent = torch.empty(n, dtype=torch.int32, device=dev)
+            out.first = torch.empty(n, dtype=torch.int32, device=dev)
+    csr = _csr_struct(offsets, targets)
+    o = _lib.PasgalBccOut(out.edge_label.data_ptr() if m else 0, out.artic_bits.data_ptr() if n else 0,
+                          out.bcc_count.data_ptr(),
+                          out.comp.data_ptr() if out.comp is not None else 0,
+                          out.parent.data_ptr() if out.parent is not None else 0,
+                          out.first.data_ptr() if out.first is not None else 0)
+    flags = _lib.PASGAL_BCC_CANONICAL if canonical else 0
+    st = lib.pasgal_bcc(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
+                        flags, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    _lib.check(st, "bcc")
+    return out
+
+
+def unpack_articulation(bits, n):
+    """uint32 bitmap (bit v&31 of word v>>5) -> bool[n]."""
+    b = np.ascontiguousarray(bits).view(np.uint8)
+    return np.unpackbits(b, bitorder="little")[:n].astype(bool)
+
+
+def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False):
+    """Drop-in for ``bcc_hopcroft_tarjan(g)``: biconnected components of a symmetric graph.
+
+    ``g`` is any object with ``offsets`` (int64[n+1]) and ``targets`` (uint32/int32/int64
+    [M]) -- a pasgal Graph, this package's Graph, or a DeviceGraph.  The CSR is copied to
+    the device, validated there (``ValueError("biconnectivity requires a symmetric graph")``
+    as in oracles.py:127-128), processed, and the labels, articulation flags and count are
+    copied back into a ``BccLabels``.  Rows must be sorted (every reference builder sorts).
+    """
+    if isinstance(g, DeviceGraph):
+        off_d, tgt_d = g.offsets, g.targets
+    else:
+        off = np.ascontiguousarray(g.offsets, dtype=np.int64)
+        tgt = np.asarray(g.targets)
+        n_host = off.shape[0] - 1
+        if n_host >= 2 ** 31 or tgt.shape[0] >= 2 ** 32:
+            raise ValueError("graph too large for int32 vertex ids / uint32 slot ids")
+        if tgt.dtype == np.uint32:
+            tgt = tgt.view(np.int32)
+        elif tgt.dtype != np.int32:
+            if tgt.shape[0] and (int(tgt.max()) >= n_host or int(tgt.min()) < 0):
+                raise ValueError("edge target out of range")
+            tgt = tgt.astype(np.int32)
+        tgt = np.ascontiguousarray(tgt)
+        off_d = torch.from_numpy(off).to(device, non_blocking=True)
+        tgt_d = torch.from_numpy(tgt).to(device, non_blocking=True)
+    n = off_d.shape[0] - 1
+    r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest)
+    lab = r.edge_label.cpu().numpy().view(np.uint32)
+    bits = r.artic_bits.cpu().numpy()
+    count = int(r.bcc_count.item())
+    art = unpack_articulation(bits, n)
+    if forest:
+        return BccLabels(art, count, edge_label=lab,
+                         comp=r.comp.cpu().numpy().astype(np.int64),
+                         parent=r.parent.cpu().numpy().astype(np.int64),
+                         first=r.first.cpu().numpy().astype(np.int64))
+    return BccLabels(art, count, edge_label=lab)

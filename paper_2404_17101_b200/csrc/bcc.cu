@@ -1,0 +1,867 @@
+// bcc.cu -- FAST-BCC on one B200 (sm_100a): the hot path behind pasgal_bcc().
+//
+// Reference contract: pasgal.oracles.bcc_hopcroft_tarjan (oracles.py:119-201) output, the
+// BccLabels parallel-mode labelling rule (results.py:76-88) and the spec'd but absent
+// parallel module `bcc`, with two corrections verified against the
+// oracle:
+//   * fence(p,v) iff first[p] <= low[v] && high[v] <= last[p]   (SPEC.md:440 tests the
+//     child's own interval, which is wrong);
+//   * skeleton = non-fence tree edges + cross edges (back edges dropped);
+//   * a non-root p is an articulation point iff some fence child c has comp[c] != comp[p]
+//     (a fence child can share p's skeleton component through a cross edge).
+//
+// Stages (kernels), all stream-ordered, no host synchronisation:
+//   S2 First-CC   k_init, k_cc_sample, k_compress, k_giant, k_cc_rest     union-find + hooks
+//   S3 rooting    k_forest_deg, scans, k_forest_fill, k_succ, list ranking (ruling set +
+//                 Wyllie on the rulers), k_tour_scatter, preorder scan     Euler tour
+//   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
+//   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_giant, k_cc2_rest
+//   S6 labels     k_compress_final, k_artic, k_labels, k_finish
+//   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
+#include <cub/block/block_reduce.cuh>
+#include "common.cuh"
+#include "scan.cuh"
+#include "tile.cuh"
+#include "../../include/pasgal_bcc.h"
+
+namespace pg {
+
+constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
+constexpr int NSAMPLE = 2;             // neighbours linked per vertex before giant detection
+constexpr u32 LR_K = 64;               // list-ranking ruler spacing (power of two)
+constexpr int GIANT_SAMPLES = 1024;
+
+struct Ctr {
+    u32 R;        // trees (roots) of the spanning forest
+    u32 giant;    // sampled largest component (First-CC)
+    u32 giant2;   // sampled largest skeleton component (Last-CC)
+    u32 ncomp;    // skeleton components
+    u32 verr;     // validation error bits
+    u32 pad[3];
+};
+
+// --------------------------------------------------------------------------
+// workspace carve-up (identical for sizing and use)
+// --------------------------------------------------------------------------
+struct Ws {
+    u32 *P, *HA, *HB, *FDEG, *FOFF, *RIDX, *ROOTS;
+    u32 *FADJ, *FTWIN, *SUCC, *RANK;
+    u32 *SPLEN[2], *SPNEXT[2];
+    u64* T;
+    uint2* FL;
+    u32 *PARENT, *PV, *E, *PPAR;
+    uint2 *W, *PM, *ST;
+    uint8_t* FEN;
+    u32* C;
+    uint2* FC;
+    u32 *ROOTMARK, *UCNT, *UOFF, *CANON;
+    u32* PART;
+    u64* SCAN;
+    Ctr* ctr;
+    i64 nb, lv, ns, ntiles;
+};
+
+static inline i64 rmq_levels(i64 nb) {
+    i64 lv = 1;
+    while (((i64)1 << lv) <= nb) ++lv;
+    return lv;
+}
+
+static size_t carve(Ws& w, char* base, i64 n, i64 m) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) -> char* {
+        o = (o + 255) & ~(size_t)255;
+        char* p = base ? base + o : nullptr;
+        o += bytes;
+        return p;
+    };
+    i64 nn = n > 0 ? n : 1;
+    i64 L = 2 * nn;
+    w.nb = cdiv(nn, 32);
+    w.lv = rmq_levels(w.nb);
+    w.ns = cdiv(L, LR_K) + 1;
+    w.ntiles = num_tiles(n, m);
+    i64 scan_items = L > m ? L : m;
+    w.P = (u32*)take(4 * nn);
+    w.HA = (u32*)take(4 * nn);
+    w.HB = (u32*)take(4 * nn);
+    w.FDEG = (u32*)take(4 * (nn + 1));
+    w.FOFF = (u32*)take(4 * (nn + 1));
+    w.RIDX = (u32*)take(4 * nn);
+    w.ROOTS = (u32*)take(4 * nn);
+    w.FADJ = (u32*)take(4 * L);
+    w.FTWIN = (u32*)take(4 * L);
+    w.SUCC = (u32*)take(4 * L);
+    w.RANK = (u32*)take(4 * L);
+    for (int b = 0; b < 2; ++b) {
+        w.SPLEN[b] = (u32*)take(4 * w.ns);
+        w.SPNEXT[b] = (u32*)take(4 * w.ns);
+    }
+    w.T = (u64*)take(8 * L);
+    w.FL = (uint2*)take(8 * nn);
+    w.PARENT = (u32*)take(4 * nn);
+    w.PV = (u32*)take(4 * nn);
+    w.E = (u32*)take(4 * nn);
+    w.PPAR = (u32*)take(4 * nn);
+    w.W = (uint2*)take(8 * nn);
+    w.PM = (uint2*)take(8 * nn);
+    w.ST = (uint2*)take(8 * w.nb * w.lv);
+    w.FEN = (uint8_t*)take(nn);
+    w.C = (u32*)take(4 * nn);
+    w.FC = (uint2*)take(8 * nn);
+    w.ROOTMARK = (u32*)take(4 * nn);
+    w.UCNT = (u32*)take(4 * nn);
+    w.UOFF = (u32*)take(4 * nn);
+    w.CANON = (u32*)take(4 * nn);
+    w.PART = (u32*)take(4 * (w.ntiles + 1));
+    w.SCAN = (u64*)take(scan_status_bytes(scan_items > nn ? scan_items : nn));
+    w.ctr = (Ctr*)take(sizeof(Ctr));
+    return o + 256;
+}
+
+// --------------------------------------------------------------------------
+// S2: First-CC (spanning forest by union-find with hook capture; Afforest-style
+// neighbour sampling, then skip the sampled giant component)
+// --------------------------------------------------------------------------
+__global__ void k_init(i64 n, u32* P, u32* HA, u32* C, u32* ROOTMARK, u32* FDEG, u32* UCNT, u32* CANON) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    P[v] = (u32)v;
+    C[v] = (u32)v;
+    HA[v] = PG_INV;
+    ROOTMARK[v] = PG_INV;
+    FDEG[v] = 0;
+    UCNT[v] = 0;
+    CANON[v] = PG_INV;
+}
+
+__global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA, u32* HB) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    i64 a = off[v], b = off[v + 1];
+    for (int k = 0; k < NSAMPLE && a + k < b; ++k) uf_link_hook(P, (u32)v, (u32)tgt[a + k], HA, HB);
+}
+
+__global__ void k_compress(i64 n, u32* P) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    u32 r = uf_find(P, (u32)v);
+    stcg(P + v, r);
+}
+
+// most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root)
+__global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u64 seed, u32* out) {
+    __shared__ u32 s[GIANT_SAMPLES];
+    typedef cub::BlockReduce<u64, GIANT_SAMPLES> BR;
+    __shared__ typename BR::TempStorage tmp;
+    int t = threadIdx.x;
+    u32 v = (u32)(draw(seed ^ 0x5EEDB1CCull, (u64)t) % (u64)n);
+    u32 r = ldcg(P + v);
+    s[t] = r;
+    __syncthreads();
+    u32 cnt = 0;
+    for (int k = 0; k < GIANT_SAMPLES; ++k) cnt += s[k] == r;
+    u64 key = ((u64)cnt << 32) | (u64)(PG_INV - r);
+    u64 best = BR(tmp).Reduce(key, cub::Max());
+    if (t == 0) *out = PG_INV - (u32)(best & 0xFFFFFFFFu);
+}
+
+__global__ void __launch_bounds__(TILE_BLOCK) k_cc_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                        i64 n, i64 m, const u32* __restrict__ part, u32* P,
+                                                        u32* HA, u32* HB, const Ctr* ctr) {
+    __shared__ TileSmem sm;
+    __shared__ uint8_t s_skip[TILE_ITEMS + 1];
+    Tile tl = tile_setup(off, n, m, part, sm);
+    const u32 giant = ctr->giant;
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_skip[r] = ldcg(P + tl.i0 + r) == giant;
+    __syncthreads();
+    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
+        int r = sm.srow[p];
+        if (s_skip[r] || p - sm.off[r] < NSAMPLE) continue;
+        uf_link_hook(P, (u32)(tl.i0 + r), (u32)tgt[tl.j0 + p], HA, HB);
+    }
+}
+
+// --------------------------------------------------------------------------
+// S3: rooting -- forest CSR, Euler tour, list ranking, preorder intervals
+// --------------------------------------------------------------------------
+__global__ void k_forest_deg(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB, u32* FDEG) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    u32 a = HA[v];
+    if (a == PG_INV) return;
+    atomicAdd(FDEG + a, 1u);
+    atomicAdd(FDEG + HB[v], 1u);
+}
+
+__global__ void k_forest_fill(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB,
+                              const u32* __restrict__ FOFF, u32* FDEG, u32* FADJ, u32* FTWIN,
+                              const u32* __restrict__ P, const u32* __restrict__ RIDX, u32* ROOTS) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    if (P[v] == (u32)v) ROOTS[RIDX[v]] = (u32)v;
+    u32 a = HA[v];
+    if (a == PG_INV) return;
+    u32 b = HB[v];
+    u32 ia = FOFF[a] + atomicSub(FDEG + a, 1u) - 1u;
+    u32 ib = FOFF[b] + atomicSub(FDEG + b, 1u) - 1u;
+    FADJ[ia] = b;
+    FTWIN[ia] = ib;
+    FADJ[ib] = a;
+    FTWIN[ib] = ia;
+}
+
+// arcs: [0, A) tree arcs in forest-CSR order; [A, 2n) virtual arcs, root q owns
+// A+2q (down into the root) and A+2q+1 (up out of the root).  Tours of consecutive roots
+// are chained, so the whole forest is one list headed by arc A.
+__global__ void k_succ(i64 n, const u32* __restrict__ FOFF, const u32* __restrict__ FADJ,
+                       const u32* __restrict__ FTWIN, const u32* __restrict__ P,
+                       const u32* __restrict__ RIDX, const u32* __restrict__ ROOTS, const Ctr* ctr, u32* SUCC) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 2 * n) return;
+    const u32 A = FOFF[n];
+    const u32 R = ctr->R;
+    u32 s;
+    if (i < A) {
+        u32 v = FADJ[i];
+        u32 nj = FTWIN[i] + 1;
+        if (nj == FOFF[v + 1]) nj = P[v] == v ? A + 2 * RIDX[v] + 1 : FOFF[v];
+        s = nj;
+    } else {
+        u32 q = (u32)(i - A) >> 1;
+        if (((i - A) & 1) == 0) {
+            u32 r = ROOTS[q];
+            s = FOFF[r + 1] > FOFF[r] ? FOFF[r] : (u32)i + 1;
+        } else {
+            s = q + 1 < R ? A + 2 * (q + 1) : PG_INV;
+        }
+    }
+    SUCC[i] = s;
+}
+
+__device__ __forceinline__ bool lr_is_ruler(u32 x, u32 head) { return (x & (LR_K - 1)) == 0 || x == head; }
+__device__ __forceinline__ u32 lr_ruler_index(u32 x, u32 nsk) { return (x & (LR_K - 1)) == 0 ? x / LR_K : nsk; }
+
+// ruler s walks its sublist: length and next ruler
+__global__ void k_lr_walk1(i64 L, i64 ns, const u32* __restrict__ SUCC, const u32* __restrict__ FOFF, i64 n,
+                           u32* SPLEN, u32* SPNEXT) {
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const u32 head = FOFF[n];
+    const u32 nsk = (u32)(ns - 1);
+    u32 e;
+    if (s < nsk) {
+        e = (u32)s * LR_K;
+    } else {
+        if ((head & (LR_K - 1)) == 0) { SPLEN[s] = 0; SPNEXT[s] = PG_INV; return; }
+        e = head;
+    }
+    u32 cnt = 0, x = e;
+    do {
+        ++cnt;
+        x = __ldg(SUCC + x);
+    } while (x != PG_INV && !lr_is_ruler(x, head));
+    SPLEN[s] = cnt;
+    SPNEXT[s] = x == PG_INV ? PG_INV : lr_ruler_index(x, nsk);
+}
+
+// Wyllie pointer jumping on the rulers: suffix sums of sublist lengths
+__global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __restrict__ nxt_in, u32* len_out, u32* nxt_out) {
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    u32 nx = nxt_in[s];
+    u32 l = len_in[s];
+    if (nx != PG_INV) {
+        l += len_in[nx];
+        nx = nxt_in[nx];
+    }
+    len_out[s] = l;
+    nxt_out[s] = nx;
+}
+
+__global__ void k_lr_walk2(i64 L, i64 ns, const u32* __restrict__ SUCC, const u32* __restrict__ FOFF, i64 n,
+                           const u32* __restrict__ SUFFIX, u32* RANK) {
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const u32 head = FOFF[n];
+    const u32 nsk = (u32)(ns - 1);
+    u32 e;
+    if (s < nsk) {
+        e = (u32)s * LR_K;
+    } else {
+        if ((head & (LR_K - 1)) == 0) return;
+        e = head;
+    }
+    u32 pos = (u32)L - SUFFIX[s], x = e;
+    do {
+        RANK[x] = pos++;
+        x = __ldg(SUCC + x);
+    } while (x != PG_INV && !lr_is_ruler(x, head));
+}
+
+// T[rank(i)] = (rank(twin(i)) << 32) | target(i) [| VFLAG for a root's down arc]
+__global__ void k_tour_scatter(i64 n, const u32* __restrict__ FOFF, const u32* __restrict__ FADJ,
+                               const u32* __restrict__ FTWIN, const u32* __restrict__ ROOTS,
+                               const u32* __restrict__ RANK, u64* T) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 2 * n) return;
+    const u32 A = FOFF[n];
+    u32 tw, tg;
+    if (i < A) {
+        tw = FTWIN[i];
+        tg = FADJ[i];
+    } else {
+        tw = (u32)i ^ 1u;  // A is even
+        tg = ROOTS[(u32)(i - A) >> 1] | ((((u32)(i - A)) & 1u) == 0 ? VFLAG : 0u);
+    }
+    T[RANK[i]] = ((u64)RANK[tw] << 32) | tg;
+}
+
+// preorder pass (fused into a decoupled-look-back scan over tour positions)
+struct PreLoad {
+    const u64* T;
+    __device__ __forceinline__ u32 operator()(i64 k) const { return (u64)k < (T[k] >> 32) ? 1u : 0u; }
+};
+struct PreStore {
+    const u64* T;
+    uint2* FL;
+    u32 *PARENT, *PV, *E, *PPAR;
+    uint2* W;
+    u32 *out_parent, *out_first;
+    __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
+        if (!down) return;
+        u64 t = T[k];
+        u32 pt = (u32)(t >> 32), lo = (u32)t;
+        u32 v = lo & ~VFLAG;
+        u32 last = f + (pt - (u32)k + 1) / 2 - 1;
+        u32 par = (lo & VFLAG) ? v : ((u32)T[k - 1] & ~VFLAG);
+        FL[v] = make_uint2(f, last);
+        PARENT[v] = par;
+        PV[f] = v;
+        E[f] = last;
+        PPAR[f] = par;
+        W[f] = make_uint2(f, f);
+        if (out_parent) out_parent[v] = par;
+        if (out_first) out_first[v] = f;
+    }
+};
+
+// --------------------------------------------------------------------------
+// S4: tags  w1/w2[first[v]] = min/max(first[v], first[u] for all neighbours u)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void warp_seg_minmax(int r, u32& mn, u32& mx, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int ro = __shfl_down_sync(0xFFFFFFFFu, r, o);
+        u32 a = __shfl_down_sync(0xFFFFFFFFu, mn, o);
+        u32 b = __shfl_down_sync(0xFFFFFFFFu, mx, o);
+        if (lane + o < 32 && ro == r) {
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TILE_BLOCK) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                     i64 n, i64 m, const u32* __restrict__ part,
+                                                     const uint2* __restrict__ FL, uint2* W) {
+    __shared__ TileSmem sm;
+    __shared__ u32 s_f[TILE_ITEMS + 1];
+    __shared__ u32 s_mn[TILE_ITEMS + 1];
+    __shared__ u32 s_mx[TILE_ITEMS + 1];
+    Tile tl = tile_setup(off, n, m, part, sm);
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
+        s_f[r] = FL[tl.i0 + r].x;
+        s_mn[r] = PG_INV;
+        s_mx[r] = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int pend = (tl.nslots + 31) & ~31;
+    // prefetch: each thread gathers all its slots' first[w] before reducing (MLP)
+    u32 fw[TILE_PER_THREAD];
+    int rr[TILE_PER_THREAD];
+#pragma unroll
+    for (int k = 0; k < TILE_PER_THREAD; ++k) {
+        int p = threadIdx.x + k * TILE_BLOCK;
+        rr[k] = p < tl.nslots ? sm.srow[p] : -1 - lane;
+        fw[k] = p < tl.nslots ? __ldg(&FL[tgt[tl.j0 + p]].x) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < TILE_PER_THREAD; ++k) {
+        int p = threadIdx.x + k * TILE_BLOCK;
+        if ((p & ~31) >= pend) break;  // warp-uniform
+        u32 mn = fw[k], mx = fw[k];
+        int r = rr[k];
+        warp_seg_minmax(r, mn, mx, lane);
+        int rprev = __shfl_up_sync(0xFFFFFFFFu, r, 1);
+        if (r >= 0 && (lane == 0 || rprev != r)) {
+            atomicMin(s_mn + r, mn);
+            atomicMax(s_mx + r, mx);
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
+        u32 mn = s_mn[r], mx = s_mx[r];
+        if (mn == PG_INV) continue;  // no slots of this row in the tile
+        u32 f = s_f[r];
+        if (tile_row_complete(sm, tl, r)) {
+            W[f] = make_uint2(mn < f ? mn : f, mx > f ? mx : f);
+        } else {
+            atomicMin(&W[f].x, mn);
+            atomicMax(&W[f].y, mx);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// S4: low/high by a blocked sparse table over preorder positions (32-wide blocks)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint2 mm(uint2 a, uint2 b) {
+    return make_uint2(a.x < b.x ? a.x : b.x, a.y > b.y ? a.y : b.y);
+}
+__device__ __forceinline__ uint2 shfl_down2(uint2 v, int o) {
+    return make_uint2(__shfl_down_sync(0xFFFFFFFFu, v.x, o), __shfl_down_sync(0xFFFFFFFFu, v.y, o));
+}
+__device__ __forceinline__ uint2 shfl_up2(uint2 v, int o) {
+    return make_uint2(__shfl_up_sync(0xFFFFFFFFu, v.x, o), __shfl_up_sync(0xFFFFFFFFu, v.y, o));
+}
+__device__ __forceinline__ uint2 shfl_idx2(uint2 v, int src) {
+    return make_uint2(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src));
+}
+
+__global__ void k_rmq_block(i64 n, const uint2* __restrict__ W, uint2* PM, uint2* ST0) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    int lane = threadIdx.x & 31;
+    uint2 v = i < n ? W[i] : make_uint2(PG_INV, 0u);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint2 u = shfl_up2(v, o);
+        if (lane >= o) v = mm(v, u);
+    }
+    if (i < n) PM[i] = v;
+    if (lane == 31 && (i >> 5) < cdiv(n, 32)) ST0[i >> 5] = v;
+}
+
+__global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i64 half) {
+    i64 b = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    uint2 v = src[b];
+    if (b + half < nb) v = mm(v, src[b + half]);
+    dst[b] = v;
+}
+
+// low/high of every preorder position, fence test, and Last-CC union of the non-fence
+// tree edges (S5 fused).
+__global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E,
+                            const u32* __restrict__ PV, const u32* __restrict__ PPAR,
+                            const uint2* __restrict__ PM, const uint2* __restrict__ ST, i64 nb,
+                            const uint2* __restrict__ FL, uint8_t* FEN, u32* C) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool valid = i < n;
+    uint2 w = valid ? W[i] : make_uint2(PG_INV, 0u);
+    u32 e = valid ? E[i] : (u32)i;
+    // in-register doubling table over [lane, lane + 2^k) within the 32-block
+    uint2 M[6];
+    M[0] = w;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) {
+        int h = 1 << (k - 1);
+        uint2 o = shfl_down2(M[k - 1], h);
+        M[k] = lane + h < 32 ? mm(M[k - 1], o) : M[k - 1];
+    }
+    uint2 sfx = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint2 u = shfl_down2(sfx, o);
+        if (lane + o < 32) sfx = mm(sfx, u);
+    }
+    const u64 bi = (u64)i >> 5, be = (u64)e >> 5;
+    const bool inblock = be == bi;
+    int kq = 0, src = lane;
+    if (inblock) {
+        u32 len = e - (u32)i + 1;
+        kq = 31 - __clz(len);
+        src = (int)(e & 31) - (1 << kq) + 1;
+    }
+    uint2 mine = M[0], far = M[0];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        uint2 t = shfl_idx2(M[k], k == kq ? src : lane);
+        if (k == kq) {
+            far = t;
+            mine = M[k];
+        }
+    }
+    if (!valid) return;
+    uint2 res;
+    if (inblock) {
+        res = mm(mine, far);
+    } else {
+        res = mm(sfx, PM[e]);
+        if (be > bi + 1) {
+            u64 l = bi + 1, r = be - 1;
+            u64 len = r - l + 1;
+            int k = 63 - __clzll((long long)len);
+            const uint2* lvl = ST + (i64)k * nb;
+            res = mm(res, mm(lvl[l], lvl[r - ((u64)1 << k) + 1]));
+        }
+    }
+    u32 v = PV[i], p = PPAR[i];
+    if (p == v) {
+        FEN[v] = 0;
+        return;
+    }
+    uint2 fp = FL[p];
+    bool fence = fp.x <= res.x && res.y <= fp.y;
+    FEN[v] = fence;
+    if (!fence) uf_link(C, v, p);
+}
+
+// --------------------------------------------------------------------------
+// S5: Last-CC over cross edges (rows outside the sampled giant skeleton component)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE_BLOCK) k_cc2_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                         i64 n, i64 m, const u32* __restrict__ part,
+                                                         const uint2* __restrict__ FL, u32* C, const Ctr* ctr) {
+    __shared__ TileSmem sm;
+    __shared__ uint8_t s_skip[TILE_ITEMS + 1];
+    __shared__ uint2 s_fl[TILE_ITEMS + 1];
+    Tile tl = tile_setup(off, n, m, part, sm);
+    const u32 giant = ctr->giant2;
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
+        bool sk = ldcg(C + tl.i0 + r) == giant;
+        s_skip[r] = sk;
+        if (!sk) s_fl[r] = FL[tl.i0 + r];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
+        int r = sm.srow[p];
+        if (s_skip[r]) continue;
+        u32 w = (u32)tgt[tl.j0 + p];
+        uint2 fu = s_fl[r], fw = FL[w];
+        bool anc = (fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y);
+        if (!anc) uf_link(C, (u32)(tl.i0 + r), w);
+    }
+}
+
+__global__ void k_compress_final(i64 n, u32* C, const uint2* __restrict__ FL, uint2* FC, Ctr* ctr, u32* out_comp) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    u32 isroot = 0;
+    if (v < n) {
+        u32 c = uf_find(C, (u32)v);
+        stcg(C + v, c);
+        FC[v] = make_uint2(FL[v].x, c);
+        if (out_comp) out_comp[v] = c;
+        isroot = c == (u32)v;
+    }
+    u32 cnt = __popc(__ballot_sync(0xFFFFFFFFu, isroot));
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr->ncomp, cnt);
+}
+
+// --------------------------------------------------------------------------
+// S6: articulation points, labels, count
+// --------------------------------------------------------------------------
+__global__ void k_artic(i64 n, const u32* __restrict__ PARENT, const uint8_t* __restrict__ FEN,
+                        const u32* __restrict__ C, u32* ROOTMARK, u32* bits) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    u32 p = PARENT[v];
+    if (p == (u32)v || !FEN[v]) return;
+    u32 cv = C[v];
+    if (cv == C[p]) return;  // fence child inside p's own skeleton component: not a head
+    if (PARENT[p] != p) {
+        atomicOr(bits + (p >> 5), 1u << (p & 31));
+    } else {
+        // root: articulation iff its head children span >= 2 skeleton components
+        u32 old = atomicCAS(ROOTMARK + p, PG_INV, cv);
+        if (old != PG_INV && old != cv) atomicOr(bits + (p >> 5), 1u << (p & 31));
+    }
+}
+
+__global__ void __launch_bounds__(TILE_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                       i64 n, i64 m, const u32* __restrict__ part,
+                                                       const uint2* __restrict__ FC, u32* label) {
+    __shared__ TileSmem sm;
+    __shared__ uint2 s_fc[TILE_ITEMS + 1];
+    Tile tl = tile_setup(off, n, m, part, sm);
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_fc[r] = FC[tl.i0 + r];
+    __syncthreads();
+    u32 w[TILE_PER_THREAD];
+    uint2 fw[TILE_PER_THREAD];
+#pragma unroll
+    for (int k = 0; k < TILE_PER_THREAD; ++k) {
+        int p = threadIdx.x + k * TILE_BLOCK;
+        w[k] = p < tl.nslots ? (u32)tgt[tl.j0 + p] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < TILE_PER_THREAD; ++k) {
+        int p = threadIdx.x + k * TILE_BLOCK;
+        fw[k] = p < tl.nslots ? __ldg(FC + w[k]) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < TILE_PER_THREAD; ++k) {
+        int p = threadIdx.x + k * TILE_BLOCK;
+        if (p >= tl.nslots) break;
+        int r = sm.srow[p];
+        uint2 fu = s_fc[r];
+        u32 u = (u32)(tl.i0 + r);
+        u32 lab = fu.x > fw[k].x ? fu.y : fw[k].y;
+        if (w[k] == u) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
+        label[tl.j0 + p] = lab;
+    }
+}
+
+__global__ void k_finish(const Ctr* ctr, i64* bcc_count) { *bcc_count = (i64)ctr->ncomp - (i64)ctr->R; }
+
+// --------------------------------------------------------------------------
+// canonical labels: min undirected edge id per BCC (results.py:103-112 equivalent)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE_BLOCK) k_canon_count(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                            i64 n, i64 m, const u32* __restrict__ part, u32* UCNT) {
+    __shared__ TileSmem sm;
+    __shared__ u32 s_c[TILE_ITEMS + 1];
+    Tile tl = tile_setup(off, n, m, part, sm);
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_c[r] = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
+        int r = sm.srow[p];
+        if ((i64)tgt[tl.j0 + p] > tl.i0 + r) atomicAdd(s_c + r, 1u);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
+        u32 c = s_c[r];
+        if (!c) continue;
+        if (tile_row_complete(sm, tl, r)) UCNT[tl.i0 + r] = c;
+        else atomicAdd(UCNT + tl.i0 + r, c);
+    }
+}
+
+__global__ void __launch_bounds__(TILE_BLOCK) k_canon_min(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                          i64 n, i64 m, const u32* __restrict__ part,
+                                                          const u32* __restrict__ UCNT, const u32* __restrict__ UOFF,
+                                                          const u32* __restrict__ label, u32* CANON) {
+    __shared__ TileSmem sm;
+    __shared__ i64 s_base[TILE_ITEMS + 1];   // eid of slot 0 of the row's upper part, minus its slot index
+    Tile tl = tile_setup(off, n, m, part, sm);
+    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
+        i64 u = tl.i0 + r;
+        s_base[r] = (i64)UOFF[u] - (off[u + 1] - (i64)UCNT[u]);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int pend = (tl.nslots + 31) & ~31;
+    for (int p = threadIdx.x; p < pend; p += TILE_BLOCK) {
+        bool up = false;
+        u32 lab = 0, eid = 0;
+        if (p < tl.nslots) {
+            int r = sm.srow[p];
+            i64 s = tl.j0 + p;
+            up = (i64)tgt[s] > tl.i0 + r;
+            if (up) {
+                eid = (u32)(s_base[r] + s);
+                lab = label[s];
+            }
+        }
+        unsigned act = __ballot_sync(0xFFFFFFFFu, up);
+        if (up) {
+            unsigned grp = __match_any_sync(act, lab);
+            // slots are in CSR order, so the lowest lane of a group carries its min eid
+            if (lane == __ffs(grp) - 1 && __ldcg(CANON + lab) > eid) atomicMin(CANON + lab, eid);
+        }
+    }
+}
+
+__global__ void k_canon_apply(i64 m, const u32* __restrict__ CANON, u32* label) {
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    u32 l = label[s];
+    if (l != PG_INV) label[s] = CANON[l];
+}
+
+struct UcntLoad {
+    const u32* UCNT;
+    __device__ __forceinline__ u32 operator()(i64 i) const { return UCNT[i]; }
+};
+struct UoffStore {
+    u32* UOFF;
+    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { UOFF[i] = ex; }
+};
+
+// deg scan -> forest offsets; root flags -> root index
+struct DegLoad {
+    const u32* FDEG;
+    __device__ __forceinline__ u32 operator()(i64 i) const { return FDEG[i]; }
+};
+struct OffStore {
+    u32* FOFF;
+    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { FOFF[i] = ex; }
+};
+struct RootLoad {
+    const u32* P;
+    __device__ __forceinline__ u32 operator()(i64 i) const { return P[i] == (u32)i ? 1u : 0u; }
+};
+struct RidxStore {
+    u32* RIDX;
+    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { RIDX[i] = ex; }
+};
+
+// --------------------------------------------------------------------------
+// validation (graph.py:87-107 ranges, graph.py:123-158 symmetry, SPEC.md:457 simple)
+// --------------------------------------------------------------------------
+constexpr u32 VERR_RANGE = 1, VERR_UNSORTED = 2, VERR_NOTSYM = 4;
+
+__global__ void k_validate_offsets(i64 n, i64 m, const i64* __restrict__ off, Ctr* ctr) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > n) return;
+    bool bad = false;
+    if (v == 0 && off[0] != 0) bad = true;
+    if (v == n && off[n] != m) bad = true;
+    if (v < n && off[v] > off[v + 1]) bad = true;
+    if (bad) atomicOr(&ctr->verr, VERR_RANGE);
+}
+
+__device__ __forceinline__ i64 lower_bound_row(const int32_t* tgt, i64 a, i64 b, int32_t key) {
+    while (a < b) {
+        i64 mid = (a + b) >> 1;
+        if (tgt[mid] < key) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(TILE_BLOCK) k_validate_slots(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                               i64 n, i64 m, const u32* __restrict__ part, Ctr* ctr) {
+    __shared__ TileSmem sm;
+    Tile tl = tile_setup(off, n, m, part, sm);
+    u32 err = 0;
+    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
+        int r = sm.srow[p];
+        i64 s = tl.j0 + p, u = tl.i0 + r;
+        int32_t w = tgt[s];
+        if (w < 0 || (i64)w >= n) { err |= VERR_RANGE; continue; }
+        i64 rs = off[u], re = off[u + 1];
+        if (s + 1 < re && tgt[s + 1] < w) { err |= VERR_UNSORTED; continue; }
+        // multiset symmetry: the k-th copy of w in row u needs a k-th copy of u in row w
+        i64 k = s - lower_bound_row(tgt, rs, s, w);
+        i64 ws = off[w], we = off[w + 1];
+        i64 q = lower_bound_row(tgt, ws, we, (int32_t)u) + k;
+        if (q >= we || tgt[q] != (int32_t)u) err |= VERR_NOTSYM;
+    }
+    if (err) atomicOr(&ctr->verr, err);
+}
+
+// --------------------------------------------------------------------------
+// host orchestration
+// --------------------------------------------------------------------------
+static inline unsigned nblk(i64 items, int bs) { return (unsigned)(items > 0 ? cdiv(items, bs) : 1); }
+
+int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr, size_t ws_bytes, u64 seed,
+               u32 flags, cudaStream_t st) {
+    const i64 n = g->n, m = g->m_slots;
+    const i64 L = 2 * n;
+    Ws w;
+    size_t need = carve(w, nullptr, n, m);
+    if (ws_bytes < need) return PASGAL_EWORKSPACE;
+    carve(w, (char*)ws_ptr, n, m);
+    const i64* off = g->offsets;
+    const int32_t* tgt = g->targets;
+    const int B = 256;
+
+    PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
+    PG_CUDA_TRY(cudaMemsetAsync(out->artic_bits, 0, sizeof(u32) * (size_t)cdiv(n, 32), st));
+    if (n == 0) {
+        k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count);
+        PG_LAUNCH_CHECK();
+        return PASGAL_OK;
+    }
+    // ---- S2 First-CC
+    k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HA, w.C, w.ROOTMARK, w.FDEG, w.UCNT, w.CANON);
+    k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(off, n, m, w.ntiles, w.PART);
+    k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB);
+    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P);
+    k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
+    if (w.ntiles > 0)
+        k_cc_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.P, w.HA, w.HB, w.ctr);
+    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P);
+    PG_LAUNCH_CHECK();
+    // ---- S3 rooting
+    k_forest_deg<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FDEG);
+    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), DegLoad{w.FDEG}, OffStore{w.FOFF}, w.FOFF + n, st));
+    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), RootLoad{w.P}, RidxStore{w.RIDX}, &w.ctr->R, st));
+    k_forest_fill<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FOFF, w.FDEG, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS);
+    k_succ<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS, w.ctr, w.SUCC);
+    k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[0], w.SPNEXT[0]);
+    int cur = 0;
+    for (i64 span = 1; span < w.ns; span <<= 1) {
+        k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]);
+        cur ^= 1;
+    }
+    k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[cur], w.RANK);
+    k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T);
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T},
+                                 PreStore{w.T, w.FL, w.PARENT, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+                                 (u32*)nullptr, st));
+    // ---- S4 tags + RMQ (+ S5 tree-edge unions)
+    if (w.ntiles > 0) k_tags<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.W);
+    k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST);
+    for (i64 k = 1; k < w.lv; ++k)
+        k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb, (i64)1 << (k - 1));
+    k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FEN, w.C);
+    PG_LAUNCH_CHECK();
+    // ---- S5 Last-CC over cross edges
+    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C);
+    k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2);
+    if (w.ntiles > 0) k_cc2_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.C, w.ctr);
+    k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp);
+    // ---- S6 articulation, labels, count
+    k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PARENT, w.FEN, w.C, w.ROOTMARK, out->artic_bits);
+    if (w.ntiles > 0) k_labels<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FC, out->edge_label);
+    k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count);
+    PG_LAUNCH_CHECK();
+    if (flags & PASGAL_BCC_CANONICAL) {
+        if (w.ntiles > 0) k_canon_count<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT);
+        PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), UcntLoad{w.UCNT}, UoffStore{w.UOFF}, (u32*)nullptr, st));
+        if (w.ntiles > 0)
+            k_canon_min<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT, w.UOFF,
+                                                                   out->edge_label, w.CANON);
+        if (m > 0) k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, out->edge_label);
+        PG_LAUNCH_CHECK();
+    }
+    return PASGAL_OK;
+}
+
+size_t bcc_workspace_bytes(i64 n, i64 m) {
+    Ws w;
+    return carve(w, nullptr, n, m);
+}
+
+int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+    const i64 n = g->n, m = g->m_slots;
+    Ws w;
+    size_t need = carve(w, nullptr, n, m);
+    if (ws_bytes < need) return PASGAL_EWORKSPACE;
+    carve(w, (char*)ws_ptr, n, m);
+    PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
+    const int B = 256;
+    k_validate_offsets<<<nblk(n + 1, B), B, 0, st>>>(n, m, g->offsets, w.ctr);
+    PG_LAUNCH_CHECK();
+    Ctr h;
+    PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
+    if (m > 0 && n > 0) {
+        k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(g->offsets, n, m, w.ntiles, w.PART);
+        k_validate_slots<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.PART, w.ctr);
+        PG_LAUNCH_CHECK();
+        PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+        PG_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
+    if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
+    if (h.verr & VERR_NOTSYM) return PASGAL_ENOTSYM;
+    return PASGAL_OK;
+}
+
+}  // namespace pg

@@ -1,0 +1,105 @@
+// capi.cu -- the extern "C" boundary declared in include/pasgal_bcc.h.
+#include "common.cuh"
+#include "../../include/pasgal_bcc.h"
+
+namespace pg {
+int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
+               cudaStream_t st);
+size_t bcc_workspace_bytes(i64 n, i64 m);
+int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gen_grid_temp_bytes(i64 rows, i64 cols);
+int gen_grid(i64 rows, i64 cols, u64 seed, u64 thr, int keep_all, i64* off, int32_t* tgt, i64* m_dev, void* temp,
+             size_t temp_bytes, cudaStream_t st);
+int gen_rmat_keys(int scale, i64 draws, u64 seed, u32 ta, u32 tab, u32 tabc, u64* keys, i64* nkeys_dev,
+                  cudaStream_t st);
+size_t gen_knn_temp_bytes(i64 npts, int gbits);
+int gen_knn_keys(i64 npts, int k, u64 seed, int gbits, u64* keys, i64* nkeys_dev, void* temp, size_t temp_bytes,
+                 cudaStream_t st);
+size_t csr_build_temp_bytes(i64 n, i64 nkeys);
+int csr_from_keys(i64 n, u64* keys, u64* keys_alt, i64 nkeys, i64* off, int32_t* tgt, i64* m_dev, void* temp,
+                  size_t temp_bytes, cudaStream_t st);
+}  // namespace pg
+
+static int check_csr(const pasgal_csr_t* g) {
+    if (!g) return PASGAL_EINVAL;
+    if (g->n < 0 || g->n >= ((int64_t)1 << 31)) return PASGAL_EINVAL;
+    if (g->m_slots < 0 || g->m_slots >= ((int64_t)1 << 32)) return PASGAL_EINVAL;
+    if (!g->offsets) return PASGAL_EINVAL;
+    if (g->m_slots > 0 && !g->targets) return PASGAL_EINVAL;
+    return PASGAL_OK;
+}
+
+extern "C" {
+
+size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots) {
+    if (n < 0) n = 0;
+    if (m_slots < 0) m_slots = 0;
+    return pg::bcc_workspace_bytes(n, m_slots);
+}
+
+int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
+               uint64_t seed, uint32_t flags, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!out || !out->bcc_count || (g->n > 0 && !out->artic_bits) || (g->m_slots > 0 && !out->edge_label))
+        return PASGAL_EINVAL;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::bcc_launch(g, out, workspace, workspace_bytes, seed, flags, (cudaStream_t)stream);
+}
+
+int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::csr_validate(g, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t pasgal_csr_build_temp_bytes(int64_t n, int64_t nkeys) { return pg::csr_build_temp_bytes(n, nkeys); }
+
+int pasgal_csr_from_keys(int64_t n, uint64_t* keys, uint64_t* keys_alt, int64_t nkeys, int64_t* offsets,
+                         int32_t* targets, int64_t* m_slots_dev, void* temp, size_t temp_bytes, void* stream) {
+    if (!offsets || !m_slots_dev || (nkeys > 0 && (!keys || !keys_alt || !targets)) || !temp) return PASGAL_EINVAL;
+    return pg::csr_from_keys(n, keys, keys_alt, nkeys, offsets, targets, m_slots_dev, temp, temp_bytes,
+                             (cudaStream_t)stream);
+}
+
+size_t pasgal_gen_grid_temp_bytes(int64_t rows, int64_t cols) { return pg::gen_grid_temp_bytes(rows, cols); }
+
+int pasgal_gen_grid(int64_t rows, int64_t cols, uint64_t seed, uint64_t keep_threshold, int keep_all,
+                    int64_t* offsets, int32_t* targets, int64_t* m_slots_dev, void* temp, size_t temp_bytes,
+                    void* stream) {
+    if (!offsets || !targets || !m_slots_dev || !temp) return PASGAL_EINVAL;
+    return pg::gen_grid(rows, cols, seed, keep_threshold, keep_all, offsets, targets, m_slots_dev, temp, temp_bytes,
+                        (cudaStream_t)stream);
+}
+
+int pasgal_gen_rmat_keys(int scale, int64_t draws, uint64_t seed, uint32_t ta, uint32_t tab, uint32_t tabc,
+                         uint64_t* keys, int64_t* nkeys_dev, void* stream) {
+    if ((draws > 0 && !keys) || !nkeys_dev || ta > tab || tab > tabc) return PASGAL_EINVAL;
+    return pg::gen_rmat_keys(scale, draws, seed, ta, tab, tabc, keys, nkeys_dev, (cudaStream_t)stream);
+}
+
+size_t pasgal_gen_knn_temp_bytes(int64_t npts, int gbits) { return pg::gen_knn_temp_bytes(npts, gbits); }
+
+int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t* keys, int64_t* nkeys_dev,
+                        void* temp, size_t temp_bytes, void* stream) {
+    if ((npts > 0 && !keys) || !nkeys_dev || !temp) return PASGAL_EINVAL;
+    return pg::gen_knn_keys(npts, k, seed, gbits, keys, nkeys_dev, temp, temp_bytes, (cudaStream_t)stream);
+}
+
+const char* pasgal_strerror(int status) {
+    switch (status) {
+        case PASGAL_OK: return "ok";
+        case PASGAL_EINVAL: return "invalid argument";
+        case PASGAL_ENOTSYM: return "biconnectivity requires a symmetric graph";
+        case PASGAL_EWORKSPACE: return "workspace too small";
+        case PASGAL_ECUDA: return "CUDA error";
+        case PASGAL_EUNSORTED: return "adjacency rows must be sorted";
+        case PASGAL_ERANGE: return "malformed CSR (offsets or target out of range)";
+        default: return "unknown status";
+    }
+}
+
+const char* pasgal_version(void) { return "pasgal-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// common.cuh -- shared device helpers for the B200-native FAST-BCC library (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int64_t i64;
+
+#define PG_INV 0xFFFFFFFFu
+
+namespace pg {
+
+// ---------------------------------------------------------------------------
+// counter-based generator hash (rules pinned in DESIGN.md "Generators")
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ u64 sm64(u64 z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ u64 draw(u64 seed, u64 ctr) { return sm64(sm64(seed) ^ ctr); }
+
+// ---------------------------------------------------------------------------
+// L2-coherent loads/stores.  Union-find parents are mutated by other SMs inside the
+// same kernel; L1 is not coherent, so parent reads bypass it (ld.global.cg).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 ldcg(const u32* p) { return __ldcg(p); }
+__device__ __forceinline__ void stcg(u32* p, u32 v) { __stcg(p, v); }
+
+__device__ __forceinline__ u64 ld_volatile_u64(const u64* p) {
+    u64 v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(u64* p, u64 v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Union-find over u32 parent arrays: link-by-index (larger root under smaller root),
+// path halving with benign racing stores.  parent[x] <= x always, so every chain is
+// strictly decreasing and halving never creates a cycle.  Each successful CAS merges two
+// distinct trees, so the edges that won a CAS form a spanning forest.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 uf_find(u32* P, u32 x) {
+    for (;;) {
+        u32 p = ldcg(P + x);
+        if (p == x) return x;
+        u32 gp = ldcg(P + p);
+        if (gp == p) return p;
+        stcg(P + x, gp);
+        x = gp;
+    }
+}
+
+// link a-b; returns true if this call merged two trees
+__device__ __forceinline__ bool uf_link(u32* P, u32 a, u32 b) {
+    u32 ra = uf_find(P, a), rb = uf_find(P, b);
+    while (ra != rb) {
+        u32 hi = ra > rb ? ra : rb, lo = ra ^ rb ^ hi;
+        u32 old = atomicCAS(P + hi, hi, lo);
+        if (old == hi) return true;
+        ra = uf_find(P, ra);
+        rb = uf_find(P, rb);
+    }
+    return false;
+}
+
+// link a-b and record the graph edge that caused the merge at the hooked root
+__device__ __forceinline__ void uf_link_hook(u32* P, u32 a, u32 b, u32* HA, u32* HB) {
+    u32 ra = uf_find(P, a), rb = uf_find(P, b);
+    while (ra != rb) {
+        u32 hi = ra > rb ? ra : rb, lo = ra ^ rb ^ hi;
+        u32 old = atomicCAS(P + hi, hi, lo);
+        if (old == hi) {
+            HA[hi] = a;
+            HB[hi] = b;
+            return;
+        }
+        ra = uf_find(P, ra);
+        rb = uf_find(P, rb);
+    }
+}
+
+__host__ __device__ __forceinline__ i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
+
+}  // namespace pg
+
+#define PG_CUDA_TRY(expr)                                  \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return PASGAL_ECUDA;        \
+    } while (0)
+
+#define PG_LAUNCH_CHECK() PG_CUDA_TRY(cudaGetLastError())

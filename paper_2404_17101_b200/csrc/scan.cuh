@@ -1,0 +1,119 @@
+// scan.cuh -- single-pass device-wide scan with decoupled look-back (sm_100a).
+//
+// One CTA per tile of SCAN_BLOCK*SCAN_IPT items; tiles are claimed through an atomic
+// counter so every predecessor of a tile is resident or finished (forward progress for
+// the look-back spin).  Each tile publishes a 64-bit status word: flag in bits 62-63
+// (0 = empty, 1 = tile aggregate, 2 = inclusive prefix) and the value in bits 0-61, so
+// flag and value land in one single-copy-atomic store and need no fence.  Values must
+// fit in 62 bits.  Load and store are functors, so a scan can be fused with its
+// producer (load) and consumer (store) -- e.g. the preorder pass of the rooting stage.
+#pragma once
+#include <cub/block/block_scan.cuh>
+#include "common.cuh"
+
+namespace pg {
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_IPT;
+constexpr u64 SCAN_VMASK = (1ull << 62) - 1;
+
+struct SumOp {
+    template <class T>
+    __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+};
+struct MinOp {
+    template <class T>
+    __device__ __forceinline__ T operator()(T a, T b) const { return a < b ? a : b; }
+};
+
+// status buffer layout: [0] = tile counter, [1 .. ntiles] = per-tile status
+inline size_t scan_status_bytes(i64 nitems) { return sizeof(u64) * (size_t)(cdiv(nitems, SCAN_TILE) + 2); }
+
+template <class T, class Op, class LoadF, class StoreF>
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan(i64 nitems, u64* status, T identity, Op op, LoadF load, StoreF store, T* total_out) {
+    typedef cub::BlockScan<T, SCAN_BLOCK> BS;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ T s_val[SCAN_TILE];
+    __shared__ T s_exc[SCAN_TILE];
+    __shared__ u32 s_tile;
+    __shared__ T s_prefix;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = (u32)atomicAdd((unsigned long long*)status, 1ull);
+    __syncthreads();
+    const i64 tile = s_tile;
+    const i64 base = tile * SCAN_TILE;
+    const i64 ntiles = cdiv(nitems, SCAN_TILE);
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        i64 idx = base + k * SCAN_BLOCK + tid;
+        s_val[k * SCAN_BLOCK + tid] = idx < nitems ? load(idx) : identity;
+    }
+    __syncthreads();
+    T v[SCAN_IPT];
+    T acc = identity;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        v[k] = s_val[tid * SCAN_IPT + k];
+        acc = op(acc, v[k]);
+    }
+    T excl, total;
+    BS(tmp).ExclusiveScan(acc, excl, identity, op, total);
+    if (tid == 0) {
+        T prefix = identity;
+        u64* st = status + 1;
+        if (tile == 0) {
+            st_volatile_u64(st, (2ull << 62) | ((u64)total & SCAN_VMASK));
+        } else {
+            st_volatile_u64(st + tile, (1ull << 62) | ((u64)total & SCAN_VMASK));
+            i64 j = tile - 1;
+            for (;;) {
+                u64 s = ld_volatile_u64(st + j);
+                u64 f = s >> 62;
+                if (f == 0) continue;
+                prefix = op((T)(s & SCAN_VMASK), prefix);
+                if (f == 2) break;
+                --j;
+            }
+            st_volatile_u64(st + tile, (2ull << 62) | ((u64)op(prefix, total) & SCAN_VMASK));
+        }
+        s_prefix = prefix;
+        if (total_out && tile == ntiles - 1) *total_out = op(prefix, total);
+    }
+    __syncthreads();
+    T run = op(s_prefix, excl);
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        s_exc[tid * SCAN_IPT + k] = run;
+        run = op(run, v[k]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        i64 idx = base + k * SCAN_BLOCK + tid;
+        if (idx < nitems) store(idx, s_exc[k * SCAN_BLOCK + tid], s_val[k * SCAN_BLOCK + tid]);
+    }
+}
+
+template <class T>
+__global__ void k_set_scalar(T* p, T v) { *p = v; }
+
+// Launch a fused scan.  `status` must hold scan_status_bytes(nitems).  For nitems == 0
+// the total (if requested) is set to the identity.
+template <class T, class Op, class LoadF, class StoreF>
+cudaError_t launch_scan(i64 nitems, u64* status, T identity, Op op, LoadF load, StoreF store,
+                        T* total_out, cudaStream_t stream) {
+    if (nitems <= 0) {
+        if (total_out) k_set_scalar<T><<<1, 1, 0, stream>>>(total_out, identity);
+        return cudaGetLastError();
+    }
+    i64 ntiles = cdiv(nitems, SCAN_TILE);
+    cudaError_t e = cudaMemsetAsync(status, 0, sizeof(u64) * (size_t)(ntiles + 1), stream);
+    if (e != cudaSuccess) return e;
+    k_scan<T, Op, LoadF, StoreF><<<(unsigned)ntiles, SCAN_BLOCK, 0, stream>>>(nitems, status, identity, op,
+                                                                                load, store, total_out);
+    return cudaGetLastError();
+}
+
+}  // namespace pg

@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a pipeline (through the C-ABI) against the oracle.
+
+Bar: bit-exact canonical labels (min undirected edge id per BCC, equivalent to the
+reference's canonical_edge_partition), identical articulation bitmap, identical
+bcc_count.  Small cases compare with the committed reference outputs
+(tests/golden/*.npz); BASELINE-sized cases compare with the C restatement of the
+reference oracle (oracle/bcc_oracle.c, itself pinned to the goldens by test_oracle.py).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+import paper_2404_17101_b200 as pg  # noqa: E402
+
+
+def _dev(case):
+    off = torch.from_numpy(np.ascontiguousarray(case.offsets)).cuda()
+    tgt = torch.from_numpy(np.ascontiguousarray(case.targets).view(np.int32)).cuda()
+    return off, tgt
+
+
+def _host_out(r, n):
+    lab = r.edge_label.cpu().numpy().view(np.uint32)
+    art = pg.unpack_articulation(r.artic_bits.cpu().numpy(), n)
+    return lab, art, int(r.bcc_count.item())
+
+
+def check_case(case, seed=0):
+    off, tgt = _dev(case)
+    r = pg.bcc_device(off, tgt, seed=seed, validate=True)
+    lab, art, cnt = _host_out(r, case.n)
+    assert cnt == case.count, f"{case.name}: bcc_count {cnt} != {case.count}"
+    assert np.array_equal(art, case.articulation), f"{case.name}: articulation differs"
+    got = pg.canonical_edge_partition(case, pg.BccLabels(art, cnt, edge_label=lab))
+    assert np.array_equal(got, case.canon), f"{case.name}: edge partition differs"
+    # canonical mode: per-slot min edge id, bit-exact with the oracle's canonicaliser
+    r2 = pg.bcc_device(off, tgt, seed=seed, canonical=True)
+    lab2, art2, cnt2 = _host_out(r2, case.n)
+    want = oracle.canonical_min_eid(case.offsets, case.targets, case.label)
+    assert np.array_equal(lab2, want), f"{case.name}: canonical labels differ"
+    assert np.array_equal(art2, case.articulation) and cnt2 == case.count
+
+
+@pytest.mark.parametrize("case", golden_io.kats(), ids=lambda c: c.name)
+def test_kats(case):
+    check_case(case)
+
+
+def test_corpus():
+    for case in golden_io.corpus():
+        check_case(case)
+
+
+@pytest.mark.parametrize("fname", golden_io.SINGLES)
+def test_golden_singles(fname):
+    check_case(golden_io.single(fname))
+
+
+def test_seed_invariance():
+    """canonical outputs do not depend on the spanning forest / seed."""
+    case = golden_io.single("c1_grid256_p06_s1.npz")
+    for seed in [0, 1, 12345, 2**63 + 7]:
+        check_case(case, seed=seed)
+
+
+def test_drop_in_call_shape():
+    """bcc(g) on a host graph returns a BccLabels the reference comparator accepts."""
+    case = golden_io.single("rmat_s12_d16_seed7.npz")
+    g = pg.Graph(case.offsets, case.targets)
+    res = pg.bcc(g)
+    assert res.bcc_count == case.count
+    assert np.array_equal(res.articulation, case.articulation)
+    assert np.array_equal(pg.canonical_edge_partition(g, res), case.canon)
+    assert res.edge_labels(g).dtype == np.int64
+    # int64 targets (the reference's from_edges keeps int64) are accepted too
+    g64 = pg.Graph(case.offsets, case.targets)
+    res64 = pg.bcc(type("G", (), {"offsets": case.offsets, "targets": case.targets.astype(np.int64)})())
+    assert np.array_equal(res64.articulation, case.articulation)
+    del g64
+
+
+def test_forest_outputs_reproduce_labels_by_reference_rule():
+    """Parallel-mode BccLabels (comp/parent/first, results.py:76-88) give the same edge
+    labels as the per-slot output, and parent/first form a valid rooted spanning forest."""
+    for case in [golden_io.single("c1_grid256_p06_s1.npz"), golden_io.single("knn_13_k5_seed3.npz")]:
+        g = pg.Graph(case.offsets, case.targets)
+        res = pg.bcc(g, forest=True)
+        par_mode = pg.BccLabels(res.articulation, res.bcc_count, comp=res._comp, parent=res._parent,
+                                first=res._first)
+        assert np.array_equal(par_mode.edge_labels(g), res.edge_labels(g))
+        first = res._first
+        assert np.array_equal(np.sort(first), np.arange(case.n))
+        parent = res._parent
+        src = np.repeat(np.arange(case.n), np.diff(case.offsets))
+        edges = set(zip(src.tolist(), case.targets.tolist()))
+        for v in range(case.n):
+            p = int(parent[v])
+            if p != v:
+                assert (v, p) in edges
+                assert first[p] < first[v]
+
+
+def test_validation_errors_match_reference():
+    # non-symmetric (oracles.py:127-128)
+    off = np.array([0, 1, 1, 1], dtype=np.int64)
+    tgt = np.array([1], dtype=np.uint32)
+    with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
+        pg.bcc(pg.Graph(off, tgt))
+    # unsorted row
+    off = np.array([0, 2, 3, 4], dtype=np.int64)
+    tgt = np.array([2, 1, 0, 0], dtype=np.uint32)
+    with pytest.raises(ValueError, match="sorted"):
+        pg.bcc(pg.Graph(off, tgt))
+    # target out of range
+    off = np.array([0, 1, 2], dtype=np.int64)
+    tgt = np.array([1, 5], dtype=np.uint32)
+    with pytest.raises(ValueError):
+        pg.bcc(pg.Graph(off, tgt))
+
+
+def test_device_generators_match_host_twins():
+    c1 = golden_io.single("c1_grid256_p06_s1.npz")
+    g = pg.gen_grid(256, 256, 0.6, 1)
+    assert np.array_equal(g.offsets.cpu().numpy(), c1.offsets)
+    assert np.array_equal(g.targets.cpu().numpy().view(np.uint32), c1.targets)
+    rm = golden_io.single("rmat_s12_d16_seed7.npz")
+    g = pg.gen_rmat(12, 1 << 16, seed=7)
+    assert np.array_equal(g.offsets.cpu().numpy(), rm.offsets)
+    assert np.array_equal(g.targets.cpu().numpy().view(np.uint32), rm.targets)
+    kn = golden_io.single("knn_13_k5_seed3.npz")
+    g = pg.gen_knn(1 << 13, 5, seed=3)
+    assert np.array_equal(g.offsets.cpu().numpy(), kn.offsets)
+    assert np.array_equal(g.targets.cpu().numpy().view(np.uint32), kn.targets)
+    # full lattice = the reference's gen_grid (graph.py:488-508)
+    kat = [c for c in golden_io.kats() if c.name == "grid10x10"][0]
+    g = pg.gen_grid(10, 10, 1.0, 0)
+    assert np.array_equal(g.offsets.cpu().numpy(), kat.offsets)
+    assert np.array_equal(g.targets.cpu().numpy().view(np.uint32), kat.targets)
+
+
+def test_device_symmetrize_matches_host():
+    rng = np.random.default_rng(5)
+    n = 5000
+    s, d = rng.integers(0, n, 40000), rng.integers(0, n, 40000)
+    g = pg.symmetrize_edges(n, s, d)
+    keys = np.concatenate([(s << 32) | d, (d << 32) | s]).astype(np.uint64)
+    off, tgt = oracle.csr_from_keys(n, keys)
+    assert np.array_equal(g.offsets.cpu().numpy(), off)
+    assert np.array_equal(g.targets.cpu().numpy().view(np.uint32), tgt)
+
+
+def _parity_device_graph(dg, seed=0):
+    """Device canonical output vs the C oracle on the same CSR (downloaded)."""
+    off = dg.offsets.cpu().numpy()
+    tgt = dg.targets.cpu().numpy().view(np.uint32)
+    r = pg.bcc_device(dg.offsets, dg.targets, seed=seed, canonical=True, validate=True)
+    lab, art, cnt = _host_out(r, dg.n)
+    ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+    want = oracle.canonical_min_eid(off, tgt, ref.edge_label)
+    assert cnt == ref.bcc_count
+    assert np.array_equal(art, ref.articulation)
+    assert np.array_equal(lab, want)
+    return cnt
+
+
+@pytest.mark.slow
+def test_config_c2_rmat_scale20():
+    dg = pg.make_config("c2")
+    hoff, htgt = oracle.rmat(20, 1 << 24, seed=1)
+    assert np.array_equal(dg.offsets.cpu().numpy(), hoff)
+    assert np.array_equal(dg.targets.cpu().numpy().view(np.uint32), htgt)
+    _parity_device_graph(dg)
+
+
+@pytest.mark.slow
+def test_config_c3_grid4096():
+    dg = pg.make_config("c3")
+    hoff, htgt = oracle.gen_grid(4096, 4096, 0.6, 1)
+    assert np.array_equal(dg.offsets.cpu().numpy(), hoff)
+    assert np.array_equal(dg.targets.cpu().numpy().view(np.uint32), htgt)
+    _parity_device_graph(dg)
+
+
+@pytest.mark.slow
+def test_config_c4_knn():
+    dg = pg.make_config("c4")
+    _parity_device_graph(dg)
+
+
+@pytest.mark.slow
+def test_large_diameter_chain_and_grid():
+    """SPEC.md:630 large-diameter smoke + a 10^6 chain (depth-independent rooting)."""
+    n = 1_000_000
+    s = np.arange(n - 1)
+    dg = pg.symmetrize_edges(n, s, s + 1)
+    cnt = _parity_device_graph(dg)
+    assert cnt == n - 1
+    dg = pg.gen_grid(2000, 2000, 1.0, 0)
+    assert _parity_device_graph(dg) == 1
