@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""bench.py -- FAST-BCC on B200: BASELINE.json's metric on its headline config.
+
+Metric: "BCC edges/sec per B200 (device-timed); achieved HBM GB/s vs ~8 TB/s peak".
+Default workload: BASELINE configs[4](a), RMAT scale 28 / 2^31 draws (avg degree 16), the
+graph the north-star target (>= 30% of HBM peak) is stated on.  One step = one FAST-BCC
+call (S2-S6: spanning forest, rooting, tags, skeleton, labels + articulation + count) over
+the device-resident CSR.  value = undirected edges processed by all ranks / max-over-ranks
+device time (CUDA events on the launching stream).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5a|c1|c2|c3|c4]
+  python bench.py --impl reference ...   # the reference CPU path (oracle port) on host cores
+
+Multi-GPU: BCC of one graph does not shard, so N>1 runs N independent
+replicas (config 5b style: each rank its own seeded instance), no collective on the data
+path; torch.distributed is used only for the barrier and the max/sum of the timings.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "BCC edges/sec per B200 (device-timed); achieved HBM GB/s vs ~8 TB/s peak"
+UNIT = "edges/s"
+L2_BYTES = 126 * 2**20
+
+# algorithmic bytes: counted once per pass that needs
+# the field, at element width, random gathers at 4 B, no credit for sector over-fetch
+def b_alg_pipeline(n, m):
+    return 56 * m + 180 * n
+
+
+KERNEL_BYTES = {
+    # k_tags: per slot target 4 + first[w] 4; per vertex offsets 8 + first[u] 4 + w1/w2 write 8
+    "tags": lambda n, m: 8 * m + 20 * n,
+    # k_labels: per slot target 4 + (first,comp)[w] 8 + label write 4; per vertex offsets 8 + (first,comp)[u] 8
+    "labels": lambda n, m: 16 * m + 16 * n,
+}
+KERNEL_NAMES = {"tags": "k_tags", "labels": "k_labels"}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def traffic_from_profiles(config, kernel):
+    """ncu dram bytes per launch for `kernel` on `config`, from the committed summary
+    (profiles/traffic.json, written from an `ncu --set full` capture), else None."""
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d[config][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------------------
+# reference arm: the reference's CPU BCC (Hopcroft-Tarjan, oracles.py:119-201) restated in
+# C (oracle/), on all host cores, on a bounded sample of the same workload
+# --------------------------------------------------------------------------------------
+
+SAMPLE_DESC = ("RMAT scale 20, 2^24 draws, (a,b,c)=(.57,.19,.19), seed 1 -- the same generator "
+               "rules as the bench workload at 1/256 of its size (= BASELINE configs[1])")
+
+
+def cpu_sample_graph(use_gpu):
+    import numpy as np
+
+    if use_gpu:
+        import paper_2404_17101_b200 as pg
+
+        dg = pg.gen_rmat(20, 1 << 24, seed=1)
+        off = dg.offsets.cpu().numpy()
+        tgt = dg.targets.cpu().numpy().view(np.uint32)
+        del dg
+        return off, tgt
+    import oracle
+
+    return oracle.rmat(20, 1 << 24, seed=1)
+
+
+def oracle_rate(off, tgt, threads=1):
+    """Run `threads` concurrent oracle instances; returns (seconds, undirected edges done)."""
+    import oracle
+
+    mu = (tgt.shape[0]) // 2
+    res = [None] * threads
+
+    def work(i):
+        t0 = time.perf_counter()
+        oracle.bcc_hopcroft_tarjan(off, tgt)
+        res[i] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return time.perf_counter() - t0, mu * threads
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    try:
+        import torch
+
+        use_gpu = torch.cuda.is_available()
+    except Exception:
+        use_gpu = False
+    off, tgt = cpu_sample_graph(use_gpu)
+    for _ in range(args.warmup):
+        oracle_rate(off, tgt, cores)
+    times, edges = [], 0
+    for _ in range(args.steps):
+        dt, e = oracle_rate(off, tgt, cores)
+        times.append(dt)
+        edges += e
+    total = sum(times)
+    value = edges / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": workload_config(args.config),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{SAMPLE_DESC}; {cores} concurrent instances per step (one per host thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name):
+    import importlib
+
+    g = importlib.import_module("paper_2404_17101_b200.graph")
+    return {"workload": f"{name}: {g.CONFIGS[name]['desc']}", "ids": "int32", "offsets": "int64"}
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_2404_17101_b200 as pg
+    from paper_2404_17101_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg_seed = pg.CONFIGS[args.config]["seed"] + rank   # independent replica per rank
+    t0 = time.perf_counter()
+    dg = pg.make_config(args.config, device=dev, seed=cfg_seed)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    torch.cuda.empty_cache()
+    n, m = dg.n, dg.m
+    mu = m // 2
+    ws = torch.empty(pg.workspace_bytes(n, m), dtype=torch.uint8, device=dev)
+    out = pg.DeviceBcc(edge_label=torch.empty(m, dtype=torch.int32, device=dev),
+                       artic_bits=torch.empty((n + 31) // 32, dtype=torch.int32, device=dev),
+                       bcc_count=torch.empty(1, dtype=torch.int64, device=dev))
+    working_set = 8 * (n + 1) + 4 * m + 4 * m + ws.numel()
+    flush = None
+    if working_set < 4 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def step(events=None):
+        return pg.bcc_device(dg.offsets, dg.targets, seed=args.seed, out=out, workspace=ws, events=events)
+
+    for _ in range(args.warmup):
+        if flush is not None:
+            flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    S = _lib.NSTAGES
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(S)] for _ in range(args.steps)]
+    launches = 0
+    sampler = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    win0 = torch.cuda.Event(enable_timing=True)
+    win1 = torch.cuda.Event(enable_timing=True)
+    win0.record()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.fill_(k)
+        r = step(evs[k])
+        launches += r.launches
+    win1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    LAB = _lib.STAGES.index("labels")
+    step_ms = [evs[k][0].elapsed_time(evs[k][LAB]) for k in range(args.steps)]
+    stage_ms = {}
+    for si in range(1, LAB + 1):
+        stage_ms[_lib.STAGES[si]] = statistics.mean(evs[k][si - 1].elapsed_time(evs[k][si]) for k in range(args.steps))
+    total_ms = sum(step_ms)
+    window_ms = win0.elapsed_time(win1)
+    edges = mu * args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e = torch.tensor([edges], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        total_ms, edges = float(t.item()), float(e.item())
+    value = edges / (total_ms / 1e3)
+
+    peak, peak_src = measured_peak()
+    # dominant kernel among the single-kernel stages
+    dom = max(KERNEL_BYTES, key=lambda s: stage_ms[s])
+    kb = KERNEL_BYTES[dom](n, m)
+    achieved = kb / (stage_ms[dom] / 1e3) / 1e9
+    pipe_bytes = b_alg_pipeline(n, m)
+    pipe_gbs = pipe_bytes / (statistics.mean(step_ms) / 1e3) / 1e9
+    traffic = traffic_from_profiles(args.config, KERNEL_NAMES[dom])
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": KERNEL_NAMES[dom],
+                "algorithmic_bytes_per_launch": kb, "kernel_ms": stage_ms[dom], "peak_source": peak_src}
+    pipeline = {"algorithmic_bytes": pipe_bytes, "model": "56*M + 180*n (SURVEY 8(d))",
+                "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
+                "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+                "stage_share": {k: round(v / statistics.mean(step_ms), 4) for k, v in stage_ms.items()}}
+
+    # ---- e2e through the public drop-in call with host buffers (pinned), H2D + D2H timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, dg, dev, n, m)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        oracle.build()
+        off_s, tgt_s = cpu_sample_graph(True)
+        dt, e = oracle_rate(off_s, tgt_s, 1)
+        cpu = {"value": e / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{SAMPLE_DESC}; one run of the C restatement of bcc_hopcroft_tarjan "
+                         f"(incl. its is_symmetric + twin passes), {dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": dict(workload_config(args.config), n=n, m_slots=m, m_undirected=mu, seed=cfg_seed,
+                           replicas=world,
+                           l2=("L2 flushed between steps (256 MB write)" if flush is not None else
+                               f"inputs larger than L2 (CSR {(8 * (n + 1) + 4 * m) / 1e9:.1f} GB)"),
+                           generation_s=round(gen_s, 2)),
+            "roofline": roofline,
+            "pipeline": pipeline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "window_ms": window_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, dg, dev, n, m):
+    """The same metric through pg.bcc(g): H2D of the CSR from pinned host memory, device
+    validation (the reference's is_symmetric), FAST-BCC, D2H of labels + articulation bitmap
+    + count into pinned host buffers -- all inside the timed region."""
+    import numpy as np
+    import torch
+
+    import paper_2404_17101_b200 as pg
+
+    off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    tgt_h = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    off_h.copy_(dg.offsets)
+    tgt_h.copy_(dg.targets)
+    g = pg.Graph(off_h.numpy(), tgt_h.numpy())
+    hb = pg.HostBuffers.allocate(n, m)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    res = pg.bcc(g, device=dev, host_out=hb)         # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = pg.bcc(g, device=dev, host_out=hb)
+    dt = (time.perf_counter() - t0) / steps
+    h2d = 8 * (n + 1) + 4 * m
+    d2h = 4 * m + 4 * ((n + 31) // 32) + 8
+    del res
+    return {"value": (m // 2) / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": dt * 1e3, "steps": steps,
+            "path": "paper_2404_17101_b200.bcc(g) with host numpy CSR (pinned) -> H2D, validate, FAST-BCC, "
+                    "D2H labels+bitmap+count (pinned)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5a", choices=["c1", "c2", "c3", "c4", "c5a"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0, help="sampling seed of the BCC call")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -81,9 +81,38 @@ size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots);
 int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace,
                size_t workspace_bytes, uint64_t seed, uint32_t flags, void* stream);
 
+/* Stage boundaries for pasgal_bcc_ex profiling: events[k] is recorded on `stream` when
+ * stage k ends (events[PASGAL_STAGE_BEGIN] when the call starts).  A single-kernel stage's
+ * elapsed time is that kernel's device duration (TAGS = k_tags, LABELS = k_labels). */
+#define PASGAL_STAGE_BEGIN 0
+#define PASGAL_STAGE_FIRST_CC 1   /* spanning forest: union-find + hook capture        */
+#define PASGAL_STAGE_FOREST 2     /* forest CSR + Euler successor                       */
+#define PASGAL_STAGE_LISTRANK 3   /* ruling-set list ranking                            */
+#define PASGAL_STAGE_TOUR 4       /* tour scatter + preorder scan (first/last/parent)   */
+#define PASGAL_STAGE_TAGS 5       /* per-slot min/max of neighbour preorder             */
+#define PASGAL_STAGE_RMQ 6        /* low/high, fence test, non-fence tree-edge unions   */
+#define PASGAL_STAGE_LAST_CC 7    /* skeleton connectivity over cross edges             */
+#define PASGAL_STAGE_ARTIC 8      /* articulation bitmap                                */
+#define PASGAL_STAGE_LABELS 9     /* per-slot labels + bcc_count                        */
+#define PASGAL_STAGE_CANONICAL 10 /* min-edge-id relabel (only with CANONICAL)          */
+#define PASGAL_BCC_NSTAGES 11
+
+typedef struct {
+    void** events;   /* cudaEvent_t[n_events] created by the caller (NULL entries skipped) */
+    int n_events;
+    int launches;    /* out: kernel launches issued by the call */
+} pasgal_bcc_prof_t;
+
+/* pasgal_bcc with optional stage events and a launch count (prof may be NULL). */
+int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace,
+                  size_t workspace_bytes, uint64_t seed, uint32_t flags, void* stream,
+                  pasgal_bcc_prof_t* prof);
+
 /* Device validation of the BCC preconditions (graph.py:87-96, 123-158):
- * offsets monotone from 0 to m_slots, targets in [0,n), rows strictly increasing (sorted,
- * no duplicates), no self-loops, and every slot u->w has its reverse w->u.
+ * offsets monotone from 0 to m_slots, targets in [0,n), rows sorted (non-decreasing), and
+ * the slot multiset closed under reversal (the k-th copy of w in row u has a k-th copy of
+ * u in row w).  Parallel edges are BCC-legal as in the reference (twin pairing); a
+ * self-loop slot is left unlabelled (0xFFFFFFFF), as the reference leaves it at -1.
  * SYNCHRONISES `stream`; returns the status (PASGAL_OK, _ERANGE, _EUNSORTED, _ENOTSYM). */
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes,
                         void* stream);

@@ -25,7 +25,7 @@ static inline uint64_t draw(uint64_t seed, uint64_t ctr) { return sm64(sm64(seed
 
 static int bits_for(int64_t n) { int b = 0; while (b < 63 && ((int64_t)1 << b) < n) ++b; return b ? b : 1; }
 
-/* Directed keys (u<<32|w) -> sorted unique -> CSR.  keys[] is clobbered.
+/* Directed keys (u<<32|w) -> sorted unique, self-loops dropped -> CSR.  keys[] is clobbered.
  * Returns M (number of slots), or -1 on OOM.  offsets[n+1] int64, targets[M] u32
  * (targets must have room for m_keys entries). */
 int64_t host_csr_from_keys(int64_t n, uint64_t* keys, int64_t m_keys,
@@ -57,6 +57,7 @@ int64_t host_csr_from_keys(int64_t n, uint64_t* keys, int64_t m_keys,
     for (int64_t i = 0; i < m_keys; ++i) {
         if (i && keys[i] == keys[i - 1]) continue;
         uint32_t u = (uint32_t)(keys[i] >> 32), w = (uint32_t)keys[i];
+        if (u == w) continue;                      /* symmetrize drops self-loops (graph.py:467-468) */
         offsets[u + 1]++;
         targets[M++] = w;
     }

@@ -27,6 +27,16 @@ class PasgalCsr(ctypes.Structure):
                 ("offsets", ctypes.c_void_p), ("targets", ctypes.c_void_p)]
 
 
+class PasgalBccProf(ctypes.Structure):
+    _fields_ = [("events", ctypes.POINTER(ctypes.c_void_p)), ("n_events", ctypes.c_int),
+                ("launches", ctypes.c_int)]
+
+
+STAGES = ["begin", "first_cc", "forest", "listrank", "tour", "tags", "rmq", "last_cc", "artic", "labels",
+          "canonical"]
+NSTAGES = len(STAGES)
+
+
 class PasgalBccOut(ctypes.Structure):
     _fields_ = [("edge_label", ctypes.c_void_p), ("artic_bits", ctypes.c_void_p),
                 ("bcc_count", ctypes.c_void_p), ("comp", ctypes.c_void_p),
@@ -44,6 +54,8 @@ _SZ = ctypes.c_size_t
 SIGNATURES = {
     "pasgal_bcc_workspace_bytes": (_SZ, [_I64, _I64]),
     "pasgal_bcc": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP]),
+    "pasgal_bcc_ex": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP,
+                             ctypes.POINTER(PasgalBccProf)]),
     "pasgal_csr_validate": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
     "pasgal_csr_build_temp_bytes": (_SZ, [_I64, _I64]),
     "pasgal_csr_from_keys": (_INT, [_I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _SZ, _VP]),

@@ -56,6 +56,7 @@ class DeviceBcc:
     comp: torch.Tensor = None   # optional int32 [n]
     parent: torch.Tensor = None
     first: torch.Tensor = None
+    launches: int = 0           # kernel launches the call issued
 
 
 def _csr_struct(offsets, targets):
@@ -78,12 +79,14 @@ def validate_device(offsets, targets, workspace=None):
 
 
 def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out=None,
-               workspace=None, forest=False):
+               workspace=None, forest=False, events=None):
     """FAST-BCC on a device CSR (offsets int64[n+1], targets int32[M], both CUDA).
 
     Returns ``DeviceBcc``.  ``canonical=True`` labels every edge with the minimum
     undirected edge id of its BCC.  ``forest=True`` also returns comp/parent/first (the
-    parallel-mode fields of BccLabels)."""
+    parallel-mode fields of BccLabels).  ``events``: optional list of
+    ``torch.cuda.Event(enable_timing=True)`` (one per stage, ``_lib.STAGES``) recorded at
+    the stage boundaries on the current stream."""
     lib = _lib.load()
     if offsets.device.type != "cuda" or targets.device.type != "cuda":
         raise ValueError("bcc_device needs CUDA tensors")
@@ -116,9 +119,20 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
                           out.parent.data_ptr() if out.parent is not None else 0,
                           out.first.data_ptr() if out.first is not None else 0)
     flags = _lib.PASGAL_BCC_CANONICAL if canonical else 0
-    st = lib.pasgal_bcc(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
-                        flags, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    stream = torch.cuda.current_stream(dev)
+    prof = _lib.PasgalBccProf(None, 0, 0)
+    if events is not None:
+        handles = []
+        for e in events:
+            if e.cuda_event == 0:       # torch creates the event lazily on first record
+                e.record(stream)
+            handles.append(e.cuda_event)
+        arr = (ctypes.c_void_p * len(handles))(*handles)
+        prof = _lib.PasgalBccProf(ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), len(handles), 0)
+    st = lib.pasgal_bcc_ex(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
+                           flags, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prof))
     _lib.check(st, "bcc")
+    out.launches = prof.launches
     return out
 
 
@@ -128,7 +142,21 @@ def unpack_articulation(bits, n):
     return np.unpackbits(b, bitorder="little")[:n].astype(bool)
 
 
-def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False):
+@dataclass
+class HostBuffers:
+    """Optional caller-owned (ideally pinned) host buffers for ``bcc(..., host_out=)``:
+    labels are copied straight into them and the returned BccLabels views them."""
+
+    edge_label: torch.Tensor    # int32 [>= M], cpu (pinned)
+    artic_bits: torch.Tensor    # int32 [>= ceil(n/32)], cpu (pinned)
+
+    @staticmethod
+    def allocate(n, m, pinned=True):
+        return HostBuffers(torch.empty(max(m, 1), dtype=torch.int32, pin_memory=pinned),
+                           torch.empty(max((n + 31) // 32, 1), dtype=torch.int32, pin_memory=pinned))
+
+
+def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False, host_out=None):
     """Drop-in for ``bcc_hopcroft_tarjan(g)``: biconnected components of a symmetric graph.
 
     ``g`` is any object with ``offsets`` (int64[n+1]) and ``targets`` (uint32/int32/int64
@@ -155,10 +183,19 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
         off_d = torch.from_numpy(off).to(device, non_blocking=True)
         tgt_d = torch.from_numpy(tgt).to(device, non_blocking=True)
     n = off_d.shape[0] - 1
+    m = tgt_d.shape[0]
     r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest)
-    lab = r.edge_label.cpu().numpy().view(np.uint32)
-    bits = r.artic_bits.cpu().numpy()
-    count = int(r.bcc_count.item())
+    if host_out is not None:
+        host_out.edge_label[:m].copy_(r.edge_label, non_blocking=True)
+        nb = (n + 31) // 32
+        host_out.artic_bits[:nb].copy_(r.artic_bits, non_blocking=True)
+        count = int(r.bcc_count.item())     # synchronises the stream
+        lab = host_out.edge_label[:m].numpy().view(np.uint32)
+        bits = host_out.artic_bits[:nb].numpy()
+    else:
+        lab = r.edge_label.cpu().numpy().view(np.uint32)
+        bits = r.artic_bits.cpu().numpy()
+        count = int(r.bcc_count.item())
     art = unpack_articulation(bits, n)
     if forest:
         return BccLabels(art, count, edge_label=lab,

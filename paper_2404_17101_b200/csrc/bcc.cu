@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(TILE_BLOCK) k_validate_slots(const i64* __rest
 static inline unsigned nblk(i64 items, int bs) { return (unsigned)(items > 0 ? cdiv(items, bs) : 1); }
 
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr, size_t ws_bytes, u64 seed,
-               u32 flags, cudaStream_t st) {
+               u32 flags, cudaStream_t st, pasgal_bcc_prof_t* prof) {
     const i64 n = g->n, m = g->m_slots;
     const i64 L = 2 * n;
     Ws w;
@@ -767,68 +767,104 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     const i64* off = g->offsets;
     const int32_t* tgt = g->targets;
     const int B = 256;
+    int nl = 0;  // kernel launches issued by this call
+    auto mark = [&](int stage) -> cudaError_t {
+        if (prof && prof->events && stage < prof->n_events && prof->events[stage])
+            return cudaEventRecord((cudaEvent_t)prof->events[stage], st);
+        return cudaSuccess;
+    };
+#define PG_K(...)        \
+    do {                 \
+        __VA_ARGS__;     \
+        ++nl;            \
+    } while (0)
 
+    PG_CUDA_TRY(mark(PASGAL_STAGE_BEGIN));
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     PG_CUDA_TRY(cudaMemsetAsync(out->artic_bits, 0, sizeof(u32) * (size_t)cdiv(n, 32), st));
     if (n == 0) {
-        k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count);
+        PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
         PG_LAUNCH_CHECK();
+        for (int s = PASGAL_STAGE_BEGIN + 1; s < PASGAL_BCC_NSTAGES; ++s) PG_CUDA_TRY(mark(s));
+        if (prof) prof->launches = nl;
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HA, w.C, w.ROOTMARK, w.FDEG, w.UCNT, w.CANON);
-    k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(off, n, m, w.ntiles, w.PART);
-    k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB);
-    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P);
-    k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
+    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HA, w.C, w.ROOTMARK, w.FDEG, w.UCNT, w.CANON));
+    PG_K(k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(off, n, m, w.ntiles, w.PART));
+    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB));
+    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
+    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     if (w.ntiles > 0)
-        k_cc_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.P, w.HA, w.HB, w.ctr);
-    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P);
+        PG_K(k_cc_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.P, w.HA, w.HB, w.ctr));
+    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting
-    k_forest_deg<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FDEG);
+    PG_K(k_forest_deg<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FDEG));
     PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), DegLoad{w.FDEG}, OffStore{w.FOFF}, w.FOFF + n, st));
     PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), RootLoad{w.P}, RidxStore{w.RIDX}, &w.ctr->R, st));
-    k_forest_fill<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FOFF, w.FDEG, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS);
-    k_succ<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS, w.ctr, w.SUCC);
-    k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[0], w.SPNEXT[0]);
+    nl += 2;
+    PG_K(k_forest_fill<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FOFF, w.FDEG, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS));
+    PG_K(k_succ<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS, w.ctr, w.SUCC));
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[0], w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
-        k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]);
+        PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[cur], w.RANK);
-    k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T);
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[cur], w.RANK));
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
+    PG_K(k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T},
                                  PreStore{w.T, w.FL, w.PARENT, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
+    ++nl;
+    PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
-    if (w.ntiles > 0) k_tags<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.W);
-    k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST);
+    if (w.ntiles > 0) PG_K(k_tags<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.W));
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
+    PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
     for (i64 k = 1; k < w.lv; ++k)
-        k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb, (i64)1 << (k - 1));
-    k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FEN, w.C);
+        PG_K(k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb, (i64)1 << (k - 1)));
+    PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FEN, w.C));
     PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
-    k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C);
-    k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2);
-    if (w.ntiles > 0) k_cc2_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.C, w.ctr);
-    k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp);
-    // ---- S6 articulation, labels, count
-    k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PARENT, w.FEN, w.C, w.ROOTMARK, out->artic_bits);
-    if (w.ntiles > 0) k_labels<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FC, out->edge_label);
-    k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count);
+    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
+    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
+    if (w.ntiles > 0)
+        PG_K(k_cc2_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.C, w.ctr));
+    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp));
     PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
+    // ---- S6 articulation, labels, count
+    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PARENT, w.FEN, w.C, w.ROOTMARK, out->artic_bits));
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
+    if (w.ntiles > 0)
+        PG_K(k_labels<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FC, out->edge_label));
+    PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
+    PG_LAUNCH_CHECK();
+    PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
     if (flags & PASGAL_BCC_CANONICAL) {
-        if (w.ntiles > 0) k_canon_count<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT);
+        if (w.ntiles > 0) PG_K(k_canon_count<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT));
         PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), UcntLoad{w.UCNT}, UoffStore{w.UOFF}, (u32*)nullptr, st));
+        ++nl;
         if (w.ntiles > 0)
-            k_canon_min<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT, w.UOFF,
-                                                                   out->edge_label, w.CANON);
-        if (m > 0) k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, out->edge_label);
+            PG_K(k_canon_min<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT, w.UOFF,
+                                                                         out->edge_label, w.CANON));
+        if (m > 0) PG_K(k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, out->edge_label));
         PG_LAUNCH_CHECK();
     }
+    PG_CUDA_TRY(mark(PASGAL_STAGE_CANONICAL));
+#undef PG_K
+    if (prof) prof->launches = nl;
     return PASGAL_OK;
 }
 

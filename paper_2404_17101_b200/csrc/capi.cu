@@ -4,7 +4,7 @@
 
 namespace pg {
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
-               cudaStream_t st);
+               cudaStream_t st, pasgal_bcc_prof_t* prof);
 size_t bcc_workspace_bytes(i64 n, i64 m);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gen_grid_temp_bytes(i64 rows, i64 cols);
@@ -37,14 +37,19 @@ size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots) {
     return pg::bcc_workspace_bytes(n, m_slots);
 }
 
-int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
-               uint64_t seed, uint32_t flags, void* stream) {
+int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
+                  uint64_t seed, uint32_t flags, void* stream, pasgal_bcc_prof_t* prof) {
     int s = check_csr(g);
     if (s) return s;
     if (!out || !out->bcc_count || (g->n > 0 && !out->artic_bits) || (g->m_slots > 0 && !out->edge_label))
         return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
-    return pg::bcc_launch(g, out, workspace, workspace_bytes, seed, flags, (cudaStream_t)stream);
+    return pg::bcc_launch(g, out, workspace, workspace_bytes, seed, flags, (cudaStream_t)stream, prof);
+}
+
+int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
+               uint64_t seed, uint32_t flags, void* stream) {
+    return pasgal_bcc_ex(g, out, workspace, workspace_bytes, seed, flags, stream, nullptr);
 }
 
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {
