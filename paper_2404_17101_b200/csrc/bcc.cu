@@ -15,7 +15,8 @@
 //   S3 rooting    k_forest_deg, scans, k_forest_fill, k_succ, list ranking (ruling set +
 //                 Wyllie on the rulers), k_tour_scatter, preorder scan     Euler tour
 //   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
-//   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_giant, k_cc2_rest
+//   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_cc2_sample, k_giant,
+//                 k_cc2_rest
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
 #include <cub/block/block_reduce.cuh>
@@ -520,8 +521,35 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 }
 
 // --------------------------------------------------------------------------
-// S5: Last-CC over cross edges (rows outside the sampled giant skeleton component)
+// S5: Last-CC over cross edges.  Sampling first (Afforest): each vertex links the first
+// NSAMPLE2 cross edges among its first SCAN2 slots, so the big skeleton component forms
+// before the sampled-giant rows are skipped by the full pass.
 // --------------------------------------------------------------------------
+constexpr int NSAMPLE2 = 2;
+constexpr int SCAN2 = 6;
+
+__device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
+    return !((fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y));
+}
+
+__global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                             const uint2* __restrict__ FL, u32* C) {
+    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    i64 a = off[u], b = off[u + 1];
+    if (a == b) return;
+    if (b > a + SCAN2) b = a + SCAN2;
+    uint2 fu = FL[u];
+    int linked = 0;
+    for (i64 s = a; s < b && linked < NSAMPLE2; ++s) {
+        u32 w = (u32)tgt[s];
+        if (is_cross(fu, FL[w])) {
+            uf_link(C, (u32)u, w);
+            ++linked;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(TILE_BLOCK) k_cc2_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                          i64 n, i64 m, const u32* __restrict__ part,
                                                          const uint2* __restrict__ FL, u32* C, const Ctr* ctr) {
@@ -540,9 +568,7 @@ __global__ void __launch_bounds__(TILE_BLOCK) k_cc2_rest(const i64* __restrict__
         int r = sm.srow[p];
         if (s_skip[r]) continue;
         u32 w = (u32)tgt[tl.j0 + p];
-        uint2 fu = s_fl[r], fw = FL[w];
-        bool anc = (fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y);
-        if (!anc) uf_link(C, (u32)(tl.i0 + r), w);
+        if (is_cross(s_fl[r], FL[w])) uf_link(C, (u32)(tl.i0 + r), w);
     }
 }
 
@@ -836,6 +862,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
+    PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     if (w.ntiles > 0)
