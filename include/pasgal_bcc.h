@@ -71,8 +71,8 @@ typedef struct {
     uint32_t* first;
 } pasgal_bcc_out_t;
 
-/* Workspace for pasgal_bcc / pasgal_csr_validate: O(n) plus O((n+m)/2048) tile
- * partition entries ("O(n) auxiliary space"). */
+/* Workspace for pasgal_bcc / pasgal_csr_validate: O(n) words plus one 4-byte row index
+ * per 256-slot warp chunk ("O(n) auxiliary space"). */
 size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots);
 
 /* FAST-BCC on a symmetric, simple CSR with sorted rows.  Asynchronous.  Input is not

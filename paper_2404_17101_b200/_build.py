@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpasgal_bcc.so")
 SOURCES = ["bcc.cu", "gen.cu", "capi.cu"]
-HEADERS = ["common.cuh", "scan.cuh", "tile.cuh"]
+HEADERS = ["common.cuh", "scan.cuh", "wchunk.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3"]

@@ -22,7 +22,7 @@
 #include <cub/block/block_reduce.cuh>
 #include "common.cuh"
 #include "scan.cuh"
-#include "tile.cuh"
+#include "wchunk.cuh"
 #include "../../include/pasgal_bcc.h"
 
 namespace pg {
@@ -50,16 +50,17 @@ struct Ws {
     u32 *SPLEN[2], *SPNEXT[2];
     u64* T;
     uint2* FL;
+    u32* FIRST;
     u32 *PARENT, *PV, *E, *PPAR;
     uint2 *W, *PM, *ST;
     uint8_t* FEN;
     u32* C;
     uint2* FC;
     u32 *ROOTMARK, *UCNT, *UOFF, *CANON;
-    u32* PART;
+    u32* CROW;
     u64* SCAN;
     Ctr* ctr;
-    i64 nb, lv, ns, ntiles;
+    i64 nb, lv, ns, nch;
 };
 
 static inline i64 rmq_levels(i64 nb) {
@@ -81,7 +82,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.nb = cdiv(nn, 32);
     w.lv = rmq_levels(w.nb);
     w.ns = cdiv(L, LR_K) + 1;
-    w.ntiles = num_tiles(n, m);
+    w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
     w.HA = (u32*)take(4 * nn);
@@ -100,6 +101,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     }
     w.T = (u64*)take(8 * L);
     w.FL = (uint2*)take(8 * nn);
+    w.FIRST = (u32*)take(4 * nn);
     w.PARENT = (u32*)take(4 * nn);
     w.PV = (u32*)take(4 * nn);
     w.E = (u32*)take(4 * nn);
@@ -114,7 +116,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.UCNT = (u32*)take(4 * nn);
     w.UOFF = (u32*)take(4 * nn);
     w.CANON = (u32*)take(4 * nn);
-    w.PART = (u32*)take(4 * (w.ntiles + 1));
+    w.CROW = (u32*)take(4 * (w.nch + 1));
     w.SCAN = (u64*)take(scan_status_bytes(scan_items > nn ? scan_items : nn));
     w.ctr = (Ctr*)take(sizeof(Ctr));
     return o + 256;
@@ -167,19 +169,23 @@ __global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u6
     if (t == 0) *out = PG_INV - (u32)(best & 0xFFFFFFFFu);
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_cc_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                        i64 n, i64 m, const u32* __restrict__ part, u32* P,
-                                                        u32* HA, u32* HB, const Ctr* ctr) {
-    __shared__ TileSmem sm;
-    __shared__ uint8_t s_skip[TILE_ITEMS + 1];
-    Tile tl = tile_setup(off, n, m, part, sm);
+__global__ void __launch_bounds__(WCH_BLOCK) k_cc_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                       i64 n, i64 m, const u32* __restrict__ crow, u32* P, u32* HA,
+                                                       u32* HB, const Ctr* ctr) {
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     const u32 giant = ctr->giant;
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_skip[r] = ldcg(P + tl.i0 + r) == giant;
-    __syncthreads();
-    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
-        int r = sm.srow[p];
-        if (s_skip[r] || p - sm.off[r] < NSAMPLE) continue;
-        uf_link_hook(P, (u32)(tl.i0 + r), (u32)tgt[tl.j0 + p], HA, HB);
+    u32 cur = crow[c];
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        if (!valid || ldcg(P + row) == giant || s - off[row] < NSAMPLE) continue;
+        uf_link_hook(P, row, (u32)tgt[s], HA, HB);
     }
 }
 
@@ -326,6 +332,7 @@ struct PreLoad {
 struct PreStore {
     const u64* T;
     uint2* FL;
+    u32* FIRST;
     u32 *PARENT, *PV, *E, *PPAR;
     uint2* W;
     u32 *out_parent, *out_first;
@@ -337,6 +344,7 @@ struct PreStore {
         u32 last = f + (pt - (u32)k + 1) / 2 - 1;
         u32 par = (lo & VFLAG) ? v : ((u32)T[k - 1] & ~VFLAG);
         FL[v] = make_uint2(f, last);
+        FIRST[v] = f;
         PARENT[v] = par;
         PV[f] = v;
         E[f] = last;
@@ -363,54 +371,46 @@ __device__ __forceinline__ void warp_seg_minmax(int r, u32& mn, u32& mx, int lan
     }
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                     i64 n, i64 m, const u32* __restrict__ part,
-                                                     const uint2* __restrict__ FL, uint2* W) {
-    __shared__ TileSmem sm;
-    __shared__ u32 s_f[TILE_ITEMS + 1];
-    __shared__ u32 s_mn[TILE_ITEMS + 1];
-    __shared__ u32 s_mx[TILE_ITEMS + 1];
-    Tile tl = tile_setup(off, n, m, part, sm);
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
-        s_f[r] = FL[tl.i0 + r].x;
-        s_mn[r] = PG_INV;
-        s_mx[r] = 0;
-    }
-    __syncthreads();
+__global__ void __launch_bounds__(WCH_BLOCK) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                    i64 n, i64 m, const u32* __restrict__ crow,
+                                                    const u32* __restrict__ FIRST, uint2* W) {
     const int lane = threadIdx.x & 31;
-    const int pend = (tl.nslots + 31) & ~31;
-    // prefetch: each thread gathers all its slots' first[w] before reducing (MLP)
-    u32 fw[TILE_PER_THREAD];
-    int rr[TILE_PER_THREAD];
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    u32 fw[WCH_U];
 #pragma unroll
-    for (int k = 0; k < TILE_PER_THREAD; ++k) {
-        int p = threadIdx.x + k * TILE_BLOCK;
-        rr[k] = p < tl.nslots ? sm.srow[p] : -1 - lane;
-        fw[k] = p < tl.nslots ? __ldg(&FL[tgt[tl.j0 + p]].x) : 0u;
+    for (int k = 0; k < WCH_U; ++k) {
+        i64 s = s0 + 32 * k + lane;
+        fw[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < TILE_PER_THREAD; ++k) {
-        int p = threadIdx.x + k * TILE_BLOCK;
-        if ((p & ~31) >= pend) break;  // warp-uniform
-        u32 mn = fw[k], mx = fw[k];
-        int r = rr[k];
-        warp_seg_minmax(r, mn, mx, lane);
-        int rprev = __shfl_up_sync(0xFFFFFFFFu, r, 1);
-        if (r >= 0 && (lane == 0 || rprev != r)) {
-            atomicMin(s_mn + r, mn);
-            atomicMax(s_mx + r, mx);
-        }
+    for (int k = 0; k < WCH_U; ++k) {
+        i64 s = s0 + 32 * k + lane;
+        if (s < s1) fw[k] = __ldg(FIRST + fw[k]);
     }
-    __syncthreads();
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
-        u32 mn = s_mn[r], mx = s_mx[r];
-        if (mn == PG_INV) continue;  // no slots of this row in the tile
-        u32 f = s_f[r];
-        if (tile_row_complete(sm, tl, r)) {
-            W[f] = make_uint2(mn < f ? mn : f, mx > f ? mx : f);
-        } else {
-            atomicMin(&W[f].x, mn);
-            atomicMax(&W[f].y, mx);
+    u32 cur = crow[c];
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) {
+        const i64 sb = s0 + 32 * k;
+        if (sb >= s1) break;  // warp-uniform
+        const bool valid = sb + lane < s1;
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        const Seg g = wc_segment(row, lane, valid, vm);
+        if (valid) {
+            u32 mn = __reduce_min_sync(g.mask, fw[k]);
+            u32 mx = __reduce_max_sync(g.mask, fw[k]);
+            if (lane == g.lo) {
+                u32 f = __ldg(FIRST + row);
+                if (!g.cut_left && !g.cut_right) {
+                    W[f] = make_uint2(mn < f ? mn : f, mx > f ? mx : f);
+                } else {
+                    atomicMin(&W[f].x, mn);
+                    atomicMax(&W[f].y, mx);
+                }
+            }
         }
     }
 }
@@ -550,25 +550,24 @@ __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* 
     }
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_cc2_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                         i64 n, i64 m, const u32* __restrict__ part,
-                                                         const uint2* __restrict__ FL, u32* C, const Ctr* ctr) {
-    __shared__ TileSmem sm;
-    __shared__ uint8_t s_skip[TILE_ITEMS + 1];
-    __shared__ uint2 s_fl[TILE_ITEMS + 1];
-    Tile tl = tile_setup(off, n, m, part, sm);
+__global__ void __launch_bounds__(WCH_BLOCK) k_cc2_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                        i64 n, i64 m, const u32* __restrict__ crow,
+                                                        const uint2* __restrict__ FL, u32* C, const Ctr* ctr) {
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     const u32 giant = ctr->giant2;
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
-        bool sk = ldcg(C + tl.i0 + r) == giant;
-        s_skip[r] = sk;
-        if (!sk) s_fl[r] = FL[tl.i0 + r];
-    }
-    __syncthreads();
-    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
-        int r = sm.srow[p];
-        if (s_skip[r]) continue;
-        u32 w = (u32)tgt[tl.j0 + p];
-        if (is_cross(s_fl[r], FL[w])) uf_link(C, (u32)(tl.i0 + r), w);
+    u32 cur = crow[c];
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        if (!valid || ldcg(C + row) == giant) continue;
+        u32 w = (u32)tgt[s];
+        if (is_cross(__ldg(FL + row), __ldg(FL + w))) uf_link(C, row, w);
     }
 }
 
@@ -606,36 +605,39 @@ __global__ void k_artic(i64 n, const u32* __restrict__ PARENT, const uint8_t* __
     }
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                       i64 n, i64 m, const u32* __restrict__ part,
-                                                       const uint2* __restrict__ FC, u32* label) {
-    __shared__ TileSmem sm;
-    __shared__ uint2 s_fc[TILE_ITEMS + 1];
-    Tile tl = tile_setup(off, n, m, part, sm);
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_fc[r] = FC[tl.i0 + r];
-    __syncthreads();
-    u32 w[TILE_PER_THREAD];
-    uint2 fw[TILE_PER_THREAD];
+__global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                      i64 n, i64 m, const u32* __restrict__ crow,
+                                                      const uint2* __restrict__ FC, u32* label) {
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    u32 w[WCH_U];
+    uint2 fw[WCH_U];
 #pragma unroll
-    for (int k = 0; k < TILE_PER_THREAD; ++k) {
-        int p = threadIdx.x + k * TILE_BLOCK;
-        w[k] = p < tl.nslots ? (u32)tgt[tl.j0 + p] : 0u;
+    for (int k = 0; k < WCH_U; ++k) {
+        i64 s = s0 + 32 * k + lane;
+        w[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < TILE_PER_THREAD; ++k) {
-        int p = threadIdx.x + k * TILE_BLOCK;
-        fw[k] = p < tl.nslots ? __ldg(FC + w[k]) : make_uint2(0u, 0u);
+    for (int k = 0; k < WCH_U; ++k) {
+        i64 s = s0 + 32 * k + lane;
+        fw[k] = s < s1 ? __ldg(FC + w[k]) : make_uint2(0u, 0u);
     }
+    u32 cur = crow[c];
 #pragma unroll
-    for (int k = 0; k < TILE_PER_THREAD; ++k) {
-        int p = threadIdx.x + k * TILE_BLOCK;
-        if (p >= tl.nslots) break;
-        int r = sm.srow[p];
-        uint2 fu = s_fc[r];
-        u32 u = (u32)(tl.i0 + r);
+    for (int k = 0; k < WCH_U; ++k) {
+        const i64 sb = s0 + 32 * k;
+        if (sb >= s1) break;  // warp-uniform
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        if (!valid) continue;
+        uint2 fu = __ldg(FC + row);
         u32 lab = fu.x > fw[k].x ? fu.y : fw[k].y;
-        if (w[k] == u) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
-        label[tl.j0 + p] = lab;
+        if (w[k] == row) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
+        __stcs(label + s, lab);
     }
 }
 
@@ -644,51 +646,54 @@ __global__ void k_finish(const Ctr* ctr, i64* bcc_count) { *bcc_count = (i64)ctr
 // --------------------------------------------------------------------------
 // canonical labels: min undirected edge id per BCC (results.py:103-112 equivalent)
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE_BLOCK) k_canon_count(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                            i64 n, i64 m, const u32* __restrict__ part, u32* UCNT) {
-    __shared__ TileSmem sm;
-    __shared__ u32 s_c[TILE_ITEMS + 1];
-    Tile tl = tile_setup(off, n, m, part, sm);
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) s_c[r] = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
-        int r = sm.srow[p];
-        if ((i64)tgt[tl.j0 + p] > tl.i0 + r) atomicAdd(s_c + r, 1u);
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
-        u32 c = s_c[r];
-        if (!c) continue;
-        if (tile_row_complete(sm, tl, r)) UCNT[tl.i0 + r] = c;
-        else atomicAdd(UCNT + tl.i0 + r, c);
+__global__ void __launch_bounds__(WCH_BLOCK) k_canon_count(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                           i64 n, i64 m, const u32* __restrict__ crow, u32* UCNT) {
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    u32 cur = crow[c];
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        const Seg g = wc_segment(row, lane, valid, vm);
+        if (valid) {
+            u32 up = (u32)tgt[s] > row ? 1u : 0u;
+            u32 cnt = __reduce_add_sync(g.mask, up);
+            if (lane == g.lo && cnt) {
+                if (!g.cut_left && !g.cut_right) UCNT[row] = cnt;
+                else atomicAdd(UCNT + row, cnt);
+            }
+        }
     }
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_canon_min(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                          i64 n, i64 m, const u32* __restrict__ part,
-                                                          const u32* __restrict__ UCNT, const u32* __restrict__ UOFF,
-                                                          const u32* __restrict__ label, u32* CANON) {
-    __shared__ TileSmem sm;
-    __shared__ i64 s_base[TILE_ITEMS + 1];   // eid of slot 0 of the row's upper part, minus its slot index
-    Tile tl = tile_setup(off, n, m, part, sm);
-    for (int r = threadIdx.x; r < tl.nrows; r += TILE_BLOCK) {
-        i64 u = tl.i0 + r;
-        s_base[r] = (i64)UOFF[u] - (off[u + 1] - (i64)UCNT[u]);
-    }
-    __syncthreads();
+__global__ void __launch_bounds__(WCH_BLOCK) k_canon_min(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                         i64 n, i64 m, const u32* __restrict__ crow,
+                                                         const u32* __restrict__ UCNT, const u32* __restrict__ UOFF,
+                                                         const u32* __restrict__ label, u32* CANON) {
     const int lane = threadIdx.x & 31;
-    const int pend = (tl.nslots + 31) & ~31;
-    for (int p = threadIdx.x; p < pend; p += TILE_BLOCK) {
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    u32 cur = crow[c];
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
         bool up = false;
         u32 lab = 0, eid = 0;
-        if (p < tl.nslots) {
-            int r = sm.srow[p];
-            i64 s = tl.j0 + p;
-            up = (i64)tgt[s] > tl.i0 + r;
-            if (up) {
-                eid = (u32)(s_base[r] + s);
-                lab = label[s];
-            }
+        if (valid && (u32)tgt[s] > row) {
+            up = true;
+            // the row's upper part is its last UCNT slots (rows are sorted)
+            eid = (u32)((i64)UOFF[row] + (s - (off[row + 1] - (i64)UCNT[row])));
+            lab = label[s];
         }
         unsigned act = __ballot_sync(0xFFFFFFFFu, up);
         if (up) {
@@ -756,14 +761,22 @@ __device__ __forceinline__ i64 lower_bound_row(const int32_t* tgt, i64 a, i64 b,
     return a;
 }
 
-__global__ void __launch_bounds__(TILE_BLOCK) k_validate_slots(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                               i64 n, i64 m, const u32* __restrict__ part, Ctr* ctr) {
-    __shared__ TileSmem sm;
-    Tile tl = tile_setup(off, n, m, part, sm);
+__global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                              i64 n, i64 m, const u32* __restrict__ crow, Ctr* ctr) {
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    u32 cur = crow[c];
     u32 err = 0;
-    for (int p = threadIdx.x; p < tl.nslots; p += TILE_BLOCK) {
-        int r = sm.srow[p];
-        i64 s = tl.j0 + p, u = tl.i0 + r;
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
+        const i64 s = sb + lane;
+        const bool valid = s < s1;
+        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+        if (!valid) continue;
+        const i64 u = row;
         int32_t w = tgt[s];
         if (w < 0 || (i64)w >= n) { err |= VERR_RANGE; continue; }
         i64 rs = off[u], re = off[u + 1];
@@ -774,7 +787,8 @@ __global__ void __launch_bounds__(TILE_BLOCK) k_validate_slots(const i64* __rest
         i64 q = lower_bound_row(tgt, ws, we, (int32_t)u) + k;
         if (q >= we || tgt[q] != (int32_t)u) err |= VERR_NOTSYM;
     }
-    if (err) atomicOr(&ctr->verr, err);
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(&ctr->verr, err);
 }
 
 // --------------------------------------------------------------------------
@@ -817,12 +831,11 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     }
     // ---- S2 First-CC
     PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HA, w.C, w.ROOTMARK, w.FDEG, w.UCNT, w.CANON));
-    PG_K(k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(off, n, m, w.ntiles, w.PART));
+    if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
-    if (w.ntiles > 0)
-        PG_K(k_cc_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.P, w.HA, w.HB, w.ctr));
+    if (w.nch > 0) PG_K(k_cc_rest<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.P, w.HA, w.HB, w.ctr));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
@@ -847,12 +860,12 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T},
-                                 PreStore{w.T, w.FL, w.PARENT, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+                                 PreStore{w.T, w.FL, w.FIRST, w.PARENT, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
-    if (w.ntiles > 0) PG_K(k_tags<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.W));
+    if (w.nch > 0) PG_K(k_tags<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
@@ -865,8 +878,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
-    if (w.ntiles > 0)
-        PG_K(k_cc2_rest<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FL, w.C, w.ctr));
+    if (w.nch > 0) PG_K(k_cc2_rest<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FL, w.C, w.ctr));
     PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
@@ -874,18 +886,17 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PARENT, w.FEN, w.C, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (w.ntiles > 0)
-        PG_K(k_labels<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.FC, out->edge_label));
+    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FC, out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
     if (flags & PASGAL_BCC_CANONICAL) {
-        if (w.ntiles > 0) PG_K(k_canon_count<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT));
+        if (w.nch > 0) PG_K(k_canon_count<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT));
         PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), UcntLoad{w.UCNT}, UoffStore{w.UOFF}, (u32*)nullptr, st));
         ++nl;
-        if (w.ntiles > 0)
-            PG_K(k_canon_min<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(off, tgt, n, m, w.PART, w.UCNT, w.UOFF,
-                                                                         out->edge_label, w.CANON));
+        if (w.nch > 0)
+            PG_K(k_canon_min<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT, w.UOFF,
+                                                                   out->edge_label, w.CANON));
         if (m > 0) PG_K(k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, out->edge_label));
         PG_LAUNCH_CHECK();
     }
@@ -915,8 +926,8 @@ int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStrea
     PG_CUDA_TRY(cudaStreamSynchronize(st));
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (m > 0 && n > 0) {
-        k_tile_partition<<<nblk(w.ntiles + 1, B), B, 0, st>>>(g->offsets, n, m, w.ntiles, w.PART);
-        k_validate_slots<<<(unsigned)w.ntiles, TILE_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.PART, w.ctr);
+        k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(g->offsets, n, m, w.nch, w.CROW);
+        k_validate_slots<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.CROW, w.ctr);
         PG_LAUNCH_CHECK();
         PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaStreamSynchronize(st));

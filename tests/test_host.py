@@ -86,14 +86,14 @@ def test_argument_checks_need_no_gpu(lib):
 
 
 def test_workspace_is_linear_in_n(lib):
-    """auxiliary space O(n); the only M-dependent part is the merge-path
-    tile partition (4 bytes per 2048 items) and the scan status (8 bytes per 2048)."""
+    """auxiliary space O(n); the only M-dependent parts are the warp-chunk
+    row partition (4 bytes per 256 slots) and the scan status (8 bytes per 2048 items)."""
     for n in [1, 1000, 1 << 20, 1 << 28]:
         base = lib.pasgal_bcc_workspace_bytes(n, 0)
         assert base <= 200 * n + (1 << 20)
         m = 50 * n
         extra = lib.pasgal_bcc_workspace_bytes(n, m) - base
-        assert extra <= 16 * (n + m) // 2048 + 4096
+        assert extra <= 4 * (m // 256 + 2) + 8 * (m // 2048 + 2) + 4096
 
 
 def test_results_mirror_matches_reference_comparator():
