@@ -7,7 +7,7 @@
 //      each, coalesced) and issues every dependent gather before it needs any result, so
 //      each lane keeps WCH_U independent HBM requests in flight;
 //   2. slot -> row: the warp holds the ends of the next 32 rows (one coalesced load of
-//      offsets) and each lane finds its row with a 5-step shuffle binary search; runs of
+//      offsets) and each lane finds its row with a 6-shuffle binary search; runs of
 //      empty rows (isolated RMAT vertices) just repeat the step 32 rows further on;
 //   3. rows are contiguous segments of lanes, so per-row reductions are one redux.sync
 //      over the segment's lane mask, and only segments cut by a window edge need atomics.
@@ -57,6 +57,7 @@ __device__ __forceinline__ u32 wc_resolve_row(const i64* __restrict__ off, i64 n
             int v = __shfl_sync(0xFFFFFFFFu, dr, pos + step - 1);
             if (v <= lane) pos += step;
         }
+        if (__shfl_sync(0xFFFFFFFFu, dr, pos) <= lane) ++pos;   // the 5 steps reach at most 31
         if (!done && pos < 32) {
             row = c + (u32)pos;
             done = true;

@@ -1,0 +1,105 @@
+"""CPU: lane-exact emulation of the warp-chunk slot->row resolution and row segmentation
+(paper_2404_17101_b200/csrc/wchunk.cuh), checked against brute force on the golden graphs
+plus CSRs dominated by empty rows (isolated vertices, as in RMAT).  Catches index
+arithmetic bugs without a GPU; the GPU parity tests check the kernels themselves."""
+
+import numpy as np
+
+from tests import golden_io
+
+WCH = 256
+
+
+def chunk_row(off, n, s):
+    lo, hi = 0, n - 1
+    while lo < hi:
+        mid = (lo + hi + 1) >> 1
+        if off[mid] <= s:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
+def resolve(off, n, cur, sb, valid):
+    rows = [0] * 32
+    done = [not v for v in valid]
+    c = cur
+    while True:
+        d = []
+        for lane in range(32):
+            e = c + 1 + lane
+            dd = int(off[e]) - sb if e <= n else 64
+            d.append(0 if dd < 0 else (33 if dd > 33 else dd))
+        for lane in range(32):
+            pos = 0
+            for step in (16, 8, 4, 2, 1):
+                if d[pos + step - 1] <= lane:
+                    pos += step
+            if d[pos] <= lane:
+                pos += 1
+            if not done[lane] and pos < 32:
+                rows[lane] = c + pos
+                done[lane] = True
+        if all(done):
+            return rows
+        c += 32
+
+
+def segments(rows, valid):
+    """(lo, hi, cut_left, cut_right) per valid lane, as wc_segment computes them."""
+    heads = 0
+    for lane in range(32):
+        if valid[lane] and (lane == 0 or rows[lane - 1] != rows[lane]):
+            heads |= 1 << lane
+    last_valid = max(i for i in range(32) if valid[i])
+    out = []
+    for lane in range(32):
+        le = (1 << (lane + 1)) - 1
+        lo = (heads & le).bit_length() - 1
+        after = heads & ~le & 0xFFFFFFFF
+        hi = ((after & -after).bit_length() - 2) if after else last_valid
+        out.append((lo, hi, lo == 0, not after))
+    return out
+
+
+def check_csr(off):
+    n = off.shape[0] - 1
+    m = int(off[-1])
+    src = np.repeat(np.arange(n), np.diff(off))
+    for c in range((m + WCH - 1) // WCH):
+        s0, s1 = c * WCH, min(c * WCH + WCH, m)
+        cur = chunk_row(off, n, s0)
+        for sb in range(s0, s1, 32):
+            valid = [sb + lane < s1 for lane in range(32)]
+            rows = resolve(off, n, cur, sb, valid)
+            cur = rows[31]
+            segs = segments(rows, valid)
+            for lane in range(32):
+                if not valid[lane]:
+                    continue
+                assert rows[lane] == src[sb + lane]
+                lo, hi, _, _ = segs[lane]
+                assert all(rows[i] == rows[lane] for i in range(lo, hi + 1))
+                assert lo == 0 or rows[lo - 1] != rows[lane]
+                assert hi == 31 or not valid[hi + 1] or rows[hi + 1] != rows[lane]
+
+
+def test_golden_graphs():
+    for case in golden_io.kats() + golden_io.corpus()[:80] + [golden_io.single("rmat_s12_d16_seed7.npz")]:
+        if case.m:
+            check_csr(case.offsets)
+
+
+def test_mostly_empty_rows():
+    rng = np.random.default_rng(1)
+    for trial in range(20):
+        n = int(rng.integers(50, 3000))
+        deg = np.where(rng.random(n) < 0.8, 0, rng.integers(1, 40, n))
+        if trial % 4 == 0:
+            deg[: n // 2] = 0                      # long run of isolated vertices
+        if trial % 5 == 0:
+            deg[int(rng.integers(0, n))] = 700     # a hub spanning several chunks
+        off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        if off[-1]:
+            check_csr(off)
