@@ -31,6 +31,7 @@ constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual 
 constexpr int NSAMPLE = 2;             // neighbours linked per vertex before giant detection
 constexpr u32 LR_K = 64;               // list-ranking ruler spacing (power of two)
 constexpr int GIANT_SAMPLES = 1024;
+constexpr int HEAVY_GRID = 148 * 4;
 
 struct Ctr {
     u32 R;        // trees (roots) of the spanning forest
@@ -38,7 +39,9 @@ struct Ctr {
     u32 giant2;   // sampled largest skeleton component (Last-CC)
     u32 ncomp;    // skeleton components
     u32 verr;     // validation error bits
-    u32 pad[3];
+    u32 nheavy;   // heavy rows queued by k_cc_rest
+    u32 nheavy2;  // heavy rows queued by k_cc2_rest
+    u32 pad;
 };
 
 // --------------------------------------------------------------------------
@@ -51,12 +54,12 @@ struct Ws {
     u64* T;
     uint2* FL;
     u32* FIRST;
-    u32 *PARENT, *PV, *E, *PPAR;
+    u32 *PV, *E, *PPAR;
     uint2 *W, *PM, *ST;
     uint8_t* FEN;
     u32* C;
     uint2* FC;
-    u32 *ROOTMARK, *UCNT, *UOFF, *CANON;
+    u32 *ROOTMARK, *UCNT, *UOFF, *CANON, *HEAVY;
     u32* CROW;
     u64* SCAN;
     Ctr* ctr;
@@ -102,7 +105,6 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.T = (u64*)take(8 * L);
     w.FL = (uint2*)take(8 * nn);
     w.FIRST = (u32*)take(4 * nn);
-    w.PARENT = (u32*)take(4 * nn);
     w.PV = (u32*)take(4 * nn);
     w.E = (u32*)take(4 * nn);
     w.PPAR = (u32*)take(4 * nn);
@@ -116,6 +118,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.UCNT = (u32*)take(4 * nn);
     w.UOFF = (u32*)take(4 * nn);
     w.CANON = (u32*)take(4 * nn);
+    w.HEAVY = (u32*)take(4 * nn);
     w.CROW = (u32*)take(4 * (w.nch + 1));
     w.SCAN = (u64*)take(scan_status_bytes(scan_items > nn ? scan_items : nn));
     w.ctr = (Ctr*)take(sizeof(Ctr));
@@ -169,49 +172,84 @@ __global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u6
     if (t == 0) *out = PG_INV - (u32)(best & 0xFFFFFFFFu);
 }
 
-__global__ void __launch_bounds__(WCH_BLOCK) k_cc_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                       i64 n, i64 m, const u32* __restrict__ crow, u32* P, u32* HA,
-                                                       u32* HB, const Ctr* ctr) {
-    const int lane = threadIdx.x & 31;
-    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
-    if (c >= num_chunks(m)) return;
-    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
-    const u32 giant = ctr->giant;
-    u32 cur = crow[c];
-#pragma unroll 1
-    for (i64 sb = s0; sb < s1; sb += 32) {
-        const i64 s = sb + lane;
-        const bool valid = s < s1;
-        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
-        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
-        if (!valid || ldcg(P + row) == giant || s - off[row] < NSAMPLE) continue;
-        uf_link_hook(P, row, (u32)tgt[s], HA, HB);
+// Rows outside the sampled giant component: a thread per vertex skips giant rows with one
+// read; rows longer than HEAVY_ROW slots go to a list served by a block per row, so a
+// stray hub never serialises on one thread.
+constexpr int HEAVY_ROW = 64;
+
+__global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA,
+                          u32* HB, Ctr* ctr, u32* heavy) {
+    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    i64 a = off[u] + NSAMPLE, b = off[u + 1];
+    if (a >= b || ldcg(P + u) == ctr->giant) return;
+    if (b - a > HEAVY_ROW) {
+        heavy[atomicAdd(&ctr->nheavy, 1u)] = (u32)u;
+        return;
+    }
+    for (i64 s = a; s < b; ++s) uf_link_hook(P, (u32)u, (u32)tgt[s], HA, HB);
+}
+
+__global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA,
+                                u32* HB, const Ctr* ctr, const u32* __restrict__ heavy) {
+    const u32 nh = ctr->nheavy;
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        u32 u = heavy[h];
+        i64 a = off[u] + NSAMPLE, b = off[u + 1];
+        for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) uf_link_hook(P, u, (u32)tgt[s], HA, HB);
     }
 }
 
 // --------------------------------------------------------------------------
 // S3: rooting -- forest CSR, Euler tour, list ranking, preorder intervals
 // --------------------------------------------------------------------------
+// Hub vertices collect many forest edges (every leaf hooked onto a hub), so the per-vertex
+// counters are warp-aggregated: lanes naming the same vertex combine into one atomic.
+__device__ __forceinline__ void agg_count(u32* cnt, u32 key, bool active) {
+    unsigned act = __ballot_sync(0xFFFFFFFFu, active);
+    if (!active) return;
+    unsigned grp = __match_any_sync(act, key);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + key, (u32)__popc(grp));
+}
+
+// returns a distinct index in [0, cnt[key]) per active lane (cnt counts down)
+__device__ __forceinline__ u32 agg_take(u32* cnt, u32 key, bool active) {
+    unsigned act = __ballot_sync(0xFFFFFFFFu, active);
+    u32 idx = 0;
+    if (active) {
+        unsigned grp = __match_any_sync(act, key);
+        int lead = __ffs(grp) - 1;
+        int lane = threadIdx.x & 31;
+        u32 base = 0;
+        if (lane == lead) base = atomicSub(cnt + key, (u32)__popc(grp)) - (u32)__popc(grp);
+        base = __shfl_sync(grp, base, lead);
+        idx = base + (u32)__popc(grp & ((1u << lane) - 1u));
+    }
+    return idx;
+}
+
 __global__ void k_forest_deg(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB, u32* FDEG) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    u32 a = HA[v];
-    if (a == PG_INV) return;
-    atomicAdd(FDEG + a, 1u);
-    atomicAdd(FDEG + HB[v], 1u);
+    u32 a = v < n ? HA[v] : PG_INV;
+    bool act = a != PG_INV;
+    u32 b = act ? HB[v] : 0u;
+    agg_count(FDEG, a, act);
+    agg_count(FDEG, b, act);
 }
 
 __global__ void k_forest_fill(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB,
                               const u32* __restrict__ FOFF, u32* FDEG, u32* FADJ, u32* FTWIN,
                               const u32* __restrict__ P, const u32* __restrict__ RIDX, u32* ROOTS) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    if (P[v] == (u32)v) ROOTS[RIDX[v]] = (u32)v;
-    u32 a = HA[v];
-    if (a == PG_INV) return;
-    u32 b = HB[v];
-    u32 ia = FOFF[a] + atomicSub(FDEG + a, 1u) - 1u;
-    u32 ib = FOFF[b] + atomicSub(FDEG + b, 1u) - 1u;
+    if (v < n && P[v] == (u32)v) ROOTS[RIDX[v]] = (u32)v;
+    u32 a = v < n ? HA[v] : PG_INV;
+    bool act = a != PG_INV;
+    u32 b = act ? HB[v] : 0u;
+    u32 ia = agg_take(FDEG, a, act);
+    u32 ib = agg_take(FDEG, b, act);
+    if (!act) return;
+    ia += FOFF[a];
+    ib += FOFF[b];
     FADJ[ia] = b;
     FTWIN[ia] = ib;
     FADJ[ib] = a;
@@ -333,7 +371,7 @@ struct PreStore {
     const u64* T;
     uint2* FL;
     u32* FIRST;
-    u32 *PARENT, *PV, *E, *PPAR;
+    u32 *PV, *E, *PPAR;
     uint2* W;
     u32 *out_parent, *out_first;
     __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
@@ -345,7 +383,6 @@ struct PreStore {
         u32 par = (lo & VFLAG) ? v : ((u32)T[k - 1] & ~VFLAG);
         FL[v] = make_uint2(f, last);
         FIRST[v] = f;
-        PARENT[v] = par;
         PV[f] = v;
         E[f] = last;
         PPAR[f] = par;
@@ -457,7 +494,7 @@ __global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i
 __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E,
                             const u32* __restrict__ PV, const u32* __restrict__ PPAR,
                             const uint2* __restrict__ PM, const uint2* __restrict__ ST, i64 nb,
-                            const uint2* __restrict__ FL, uint8_t* FEN, u32* C) {
+                            const uint2* __restrict__ FL, uint8_t* FEN /* [first] */, u32* C) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool valid = i < n;
@@ -510,14 +547,13 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
         }
     }
     u32 v = PV[i], p = PPAR[i];
-    if (p == v) {
-        FEN[v] = 0;
-        return;
+    bool fence = false;
+    if (p != v) {
+        uint2 fp = FL[p];
+        fence = fp.x <= res.x && res.y <= fp.y;
+        if (!fence) uf_link(C, v, p);
     }
-    uint2 fp = FL[p];
-    bool fence = fp.x <= res.x && res.y <= fp.y;
-    FEN[v] = fence;
-    if (!fence) uf_link(C, v, p);
+    FEN[i] = fence;  // preorder space: coalesced
 }
 
 // --------------------------------------------------------------------------
@@ -550,24 +586,34 @@ __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* 
     }
 }
 
-__global__ void __launch_bounds__(WCH_BLOCK) k_cc2_rest(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                        i64 n, i64 m, const u32* __restrict__ crow,
-                                                        const uint2* __restrict__ FL, u32* C, const Ctr* ctr) {
-    const int lane = threadIdx.x & 31;
-    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
-    if (c >= num_chunks(m)) return;
-    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
-    const u32 giant = ctr->giant2;
-    u32 cur = crow[c];
-#pragma unroll 1
-    for (i64 sb = s0; sb < s1; sb += 32) {
-        const i64 s = sb + lane;
-        const bool valid = s < s1;
-        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
-        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
-        if (!valid || ldcg(C + row) == giant) continue;
+// tree roots have only back edges (every vertex of the tree descends from the root)
+__global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                           const uint2* __restrict__ FL, const u32* __restrict__ P, u32* C, Ctr* ctr, u32* heavy) {
+    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    i64 a = off[u], b = off[u + 1];
+    if (a >= b || P[u] == (u32)u || ldcg(C + u) == ctr->giant2) return;
+    if (b - a > HEAVY_ROW) {
+        heavy[atomicAdd(&ctr->nheavy2, 1u)] = (u32)u;
+        return;
+    }
+    uint2 fu = FL[u];
+    for (i64 s = a; s < b; ++s) {
         u32 w = (u32)tgt[s];
-        if (is_cross(__ldg(FL + row), __ldg(FL + w))) uf_link(C, row, w);
+        if (is_cross(fu, FL[w])) uf_link(C, (u32)u, w);
+    }
+}
+
+__global__ void k_cc2_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                 const uint2* __restrict__ FL, u32* C, const Ctr* ctr, const u32* __restrict__ heavy) {
+    const u32 nh = ctr->nheavy2;
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        u32 u = heavy[h];
+        uint2 fu = FL[u];
+        for (i64 s = off[u] + threadIdx.x; s < off[u + 1]; s += blockDim.x) {
+            u32 w = (u32)tgt[s];
+            if (is_cross(fu, FL[w])) uf_link(C, u, w);
+        }
     }
 }
 
@@ -588,18 +634,21 @@ __global__ void k_compress_final(i64 n, u32* C, const uint2* __restrict__ FL, ui
 // --------------------------------------------------------------------------
 // S6: articulation points, labels, count
 // --------------------------------------------------------------------------
-__global__ void k_artic(i64 n, const u32* __restrict__ PARENT, const uint8_t* __restrict__ FEN,
-                        const u32* __restrict__ C, u32* ROOTMARK, u32* bits) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    u32 p = PARENT[v];
-    if (p == (u32)v || !FEN[v]) return;
+// articulation, in preorder space (position i = first[v]): every vertex whose tree edge is
+// a fence and whose skeleton component differs from its parent's heads a BCC hanging off
+// the parent; a non-root parent is then an articulation point, a root only if its head
+// children span >= 2 components.  P (First-CC) has P[x] == x exactly at tree roots.
+__global__ void k_artic(i64 n, const u32* __restrict__ PV, const u32* __restrict__ PPAR,
+                        const uint8_t* __restrict__ FEN, const u32* __restrict__ C, const u32* __restrict__ P,
+                        u32* ROOTMARK, u32* bits) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !FEN[i]) return;
+    u32 v = PV[i], p = PPAR[i];
     u32 cv = C[v];
     if (cv == C[p]) return;  // fence child inside p's own skeleton component: not a head
-    if (PARENT[p] != p) {
+    if (P[p] != p) {
         atomicOr(bits + (p >> 5), 1u << (p & 31));
     } else {
-        // root: articulation iff its head children span >= 2 skeleton components
         u32 old = atomicCAS(ROOTMARK + p, PG_INV, cv);
         if (old != PG_INV && old != cv) atomicOr(bits + (p >> 5), 1u << (p & 31));
     }
@@ -835,7 +884,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
-    if (w.nch > 0) PG_K(k_cc_rest<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.P, w.HA, w.HB, w.ctr));
+    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB, w.ctr, w.HEAVY));
+    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HA, w.HB, w.ctr, w.HEAVY));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
@@ -860,7 +910,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T},
-                                 PreStore{w.T, w.FL, w.FIRST, w.PARENT, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+                                 PreStore{w.T, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
@@ -878,12 +928,13 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
-    if (w.nch > 0) PG_K(k_cc2_rest<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FL, w.C, w.ctr));
+    PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.P, w.C, w.ctr, w.HEAVY));
+    PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
     PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
     // ---- S6 articulation, labels, count
-    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PARENT, w.FEN, w.C, w.ROOTMARK, out->artic_bits));
+    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PV, w.PPAR, w.FEN, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
     if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FC, out->edge_label));
