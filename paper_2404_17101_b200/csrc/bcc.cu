@@ -2,8 +2,8 @@
 //
 // Reference contract: pasgal.oracles.bcc_hopcroft_tarjan (oracles.py:119-201) output, the
 // BccLabels parallel-mode labelling rule (results.py:76-88) and the spec'd but absent
-// parallel module `bcc`, with two corrections verified against the
-// oracle:
+// parallel module `bcc`, with corrections verified against the oracle
+// (DESIGN.md section 3):
 //   * fence(p,v) iff first[p] <= low[v] && high[v] <= last[p]   (SPEC.md:440 tests the
 //     child's own interval, which is wrong);
 //   * skeleton = non-fence tree edges + cross edges (back edges dropped);
@@ -11,12 +11,13 @@
 //     (a fence child can share p's skeleton component through a cross edge).
 //
 // Stages (kernels), all stream-ordered, no host synchronisation:
-//   S2 First-CC   k_init, k_cc_sample, k_compress, k_giant, k_cc_rest     union-find + hooks
-//   S3 rooting    k_forest_deg, scans, k_forest_fill, k_succ, list ranking (ruling set +
-//                 Wyllie on the rulers), k_tour_scatter, preorder scan     Euler tour
+//   S2 First-CC   k_init, k_chunk_rows, k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
+//                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
+//   S3 rooting    root scan, k_arc_link, k_arc_close, ruling-set list ranking (k_lr_walk1,
+//                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
 //   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_cc2_sample, k_giant,
-//                 k_cc2_rest
+//                 k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
 #include <cub/block/block_reduce.cuh>
@@ -48,8 +49,9 @@ struct Ctr {
 // workspace carve-up (identical for sizing and use)
 // --------------------------------------------------------------------------
 struct Ws {
-    u32 *P, *HA, *HB, *FDEG, *FOFF, *RIDX, *ROOTS;
-    u32 *FADJ, *FTWIN, *SUCC, *RANK;
+    u32 *P, *HEAD, *RIDX, *ROOTS;
+    uint2* HAB;
+    u32 *NEXT, *RANK;
     u32 *SPLEN[2], *SPNEXT[2];
     u64* T;
     uint2* FL;
@@ -84,19 +86,15 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     i64 L = 2 * nn;
     w.nb = cdiv(nn, 32);
     w.lv = rmq_levels(w.nb);
-    w.ns = cdiv(L, LR_K) + 1;
+    w.ns = cdiv(L, LR_K);
     w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
-    w.HA = (u32*)take(4 * nn);
-    w.HB = (u32*)take(4 * nn);
-    w.FDEG = (u32*)take(4 * (nn + 1));
-    w.FOFF = (u32*)take(4 * (nn + 1));
+    w.HAB = (uint2*)take(8 * nn);
+    w.HEAD = (u32*)take(4 * nn);
     w.RIDX = (u32*)take(4 * nn);
     w.ROOTS = (u32*)take(4 * nn);
-    w.FADJ = (u32*)take(4 * L);
-    w.FTWIN = (u32*)take(4 * L);
-    w.SUCC = (u32*)take(4 * L);
+    w.NEXT = (u32*)take(4 * L);
     w.RANK = (u32*)take(4 * L);
     for (int b = 0; b < 2; ++b) {
         w.SPLEN[b] = (u32*)take(4 * w.ns);
@@ -129,23 +127,23 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
 // S2: First-CC (spanning forest by union-find with hook capture; Afforest-style
 // neighbour sampling, then skip the sampled giant component)
 // --------------------------------------------------------------------------
-__global__ void k_init(i64 n, u32* P, u32* HA, u32* C, u32* ROOTMARK, u32* FDEG, u32* UCNT, u32* CANON) {
+__global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C, u32* ROOTMARK, u32* UCNT, u32* CANON) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     P[v] = (u32)v;
     C[v] = (u32)v;
-    HA[v] = PG_INV;
+    HAB[v] = make_uint2(PG_INV, PG_INV);
+    HEAD[v] = PG_INV;
     ROOTMARK[v] = PG_INV;
-    FDEG[v] = 0;
     UCNT[v] = 0;
     CANON[v] = PG_INV;
 }
 
-__global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA, u32* HB) {
+__global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     i64 a = off[v], b = off[v + 1];
-    for (int k = 0; k < NSAMPLE && a + k < b; ++k) uf_link_hook(P, (u32)v, (u32)tgt[a + k], HA, HB);
+    for (int k = 0; k < NSAMPLE && a + k < b; ++k) uf_link_hook(P, (u32)v, (u32)tgt[a + k], HAB);
 }
 
 __global__ void k_compress(i64 n, u32* P) {
@@ -177,8 +175,8 @@ __global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u6
 // stray hub never serialises on one thread.
 constexpr int HEAVY_ROW = 64;
 
-__global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA,
-                          u32* HB, Ctr* ctr, u32* heavy) {
+__global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                          Ctr* ctr, u32* heavy) {
     i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n) return;
     i64 a = off[u] + NSAMPLE, b = off[u + 1];
@@ -187,131 +185,112 @@ __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __r
         heavy[atomicAdd(&ctr->nheavy, 1u)] = (u32)u;
         return;
     }
-    for (i64 s = a; s < b; ++s) uf_link_hook(P, (u32)u, (u32)tgt[s], HA, HB);
+    for (i64 s = a; s < b; ++s) uf_link_hook(P, (u32)u, (u32)tgt[s], HAB);
 }
 
-__global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, u32* HA,
-                                u32* HB, const Ctr* ctr, const u32* __restrict__ heavy) {
+__global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                                const Ctr* ctr, const u32* __restrict__ heavy) {
     const u32 nh = ctr->nheavy;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         u32 u = heavy[h];
         i64 a = off[u] + NSAMPLE, b = off[u + 1];
-        for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) uf_link_hook(P, u, (u32)tgt[s], HA, HB);
+        for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) uf_link_hook(P, u, (u32)tgt[s], HAB);
     }
 }
 
 // --------------------------------------------------------------------------
-// S3: rooting -- forest CSR, Euler tour, list ranking, preorder intervals
+// S3: rooting by an Euler tour of the spanning forest.
+//
+// Arc space [0, 2n): a hooked vertex x owns the two arcs of its forest edge HAB[x]={a,b}:
+// 2x = a->b and 2x+1 = b->a, so twin(arc) = arc^1.  A root r (never hooked) owns its two
+// virtual arcs: 2r = down into r, 2r+1 = up out of r.  Around every vertex the out-arcs
+// form a circular list NEXT (built with warp-aggregated atomicExch on HEAD[v]); the tour
+// successor is then uniformly succ(arc) = NEXT[arc^1].  A root's cycle is cut at its up
+// arc and consecutive roots are chained, so the forest is one list headed by arc 0
+// (vertex 0 is always a root: union by index keeps the minimum id as the root).
 // --------------------------------------------------------------------------
-// Hub vertices collect many forest edges (every leaf hooked onto a hub), so the per-vertex
-// counters are warp-aggregated: lanes naming the same vertex combine into one atomic.
-__device__ __forceinline__ void agg_count(u32* cnt, u32 key, bool active) {
+
+// Insert `arc` at the head of key's circular out-arc list.  Lanes naming the same key
+// (hubs) are chained locally and spliced in with one atomicExch.
+__device__ __forceinline__ void arc_push(u32* HEAD, u32* NEXT, u32 key, u32 arc, bool active) {
     unsigned act = __ballot_sync(0xFFFFFFFFu, active);
     if (!active) return;
+    const int lane = threadIdx.x & 31;
     unsigned grp = __match_any_sync(act, key);
-    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + key, (u32)__popc(grp));
+    int lead = __ffs(grp) - 1;
+    u32 old = 0;
+    if (lane == lead) old = atomicExch(HEAD + key, arc);
+    old = __shfl_sync(grp, old, lead);
+    unsigned later = grp & (lane == 31 ? 0u : (0xFFFFFFFEu << lane));
+    u32 nxt_arc = __shfl_sync(grp, arc, later ? __ffs(later) - 1 : lane);
+    NEXT[arc] = later ? nxt_arc : old;   // the group's last arc continues into the old list
 }
 
-// returns a distinct index in [0, cnt[key]) per active lane (cnt counts down)
-__device__ __forceinline__ u32 agg_take(u32* cnt, u32 key, bool active) {
-    unsigned act = __ballot_sync(0xFFFFFFFFu, active);
-    u32 idx = 0;
-    if (active) {
-        unsigned grp = __match_any_sync(act, key);
-        int lead = __ffs(grp) - 1;
-        int lane = threadIdx.x & 31;
-        u32 base = 0;
-        if (lane == lead) base = atomicSub(cnt + key, (u32)__popc(grp)) - (u32)__popc(grp);
-        base = __shfl_sync(grp, base, lead);
-        idx = base + (u32)__popc(grp & ((1u << lane) - 1u));
-    }
-    return idx;
+__global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
+    i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    uint2 e = x < n ? HAB[x] : make_uint2(PG_INV, PG_INV);
+    bool act = e.x != PG_INV;
+    arc_push(HEAD, NEXT, e.x, 2 * (u32)x, act);       // a -> b is an out-arc of a
+    arc_push(HEAD, NEXT, e.y, 2 * (u32)x + 1, act);   // b -> a is an out-arc of b
 }
 
-__global__ void k_forest_deg(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB, u32* FDEG) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    u32 a = v < n ? HA[v] : PG_INV;
-    bool act = a != PG_INV;
-    u32 b = act ? HB[v] : 0u;
-    agg_count(FDEG, a, act);
-    agg_count(FDEG, b, act);
-}
-
-__global__ void k_forest_fill(i64 n, const u32* __restrict__ HA, const u32* __restrict__ HB,
-                              const u32* __restrict__ FOFF, u32* FDEG, u32* FADJ, u32* FTWIN,
-                              const u32* __restrict__ P, const u32* __restrict__ RIDX, u32* ROOTS) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n && P[v] == (u32)v) ROOTS[RIDX[v]] = (u32)v;
-    u32 a = v < n ? HA[v] : PG_INV;
-    bool act = a != PG_INV;
-    u32 b = act ? HB[v] : 0u;
-    u32 ia = agg_take(FDEG, a, act);
-    u32 ib = agg_take(FDEG, b, act);
-    if (!act) return;
-    ia += FOFF[a];
-    ib += FOFF[b];
-    FADJ[ia] = b;
-    FTWIN[ia] = ib;
-    FADJ[ib] = a;
-    FTWIN[ib] = ia;
-}
-
-// arcs: [0, A) tree arcs in forest-CSR order; [A, 2n) virtual arcs, root q owns
-// A+2q (down into the root) and A+2q+1 (up out of the root).  Tours of consecutive roots
-// are chained, so the whole forest is one list headed by arc A.
-__global__ void k_succ(i64 n, const u32* __restrict__ FOFF, const u32* __restrict__ FADJ,
-                       const u32* __restrict__ FTWIN, const u32* __restrict__ P,
-                       const u32* __restrict__ RIDX, const u32* __restrict__ ROOTS, const Ctr* ctr, u32* SUCC) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 2 * n) return;
-    const u32 A = FOFF[n];
-    const u32 R = ctr->R;
-    u32 s;
-    if (i < A) {
-        u32 v = FADJ[i];
-        u32 nj = FTWIN[i] + 1;
-        if (nj == FOFF[v + 1]) nj = P[v] == v ? A + 2 * RIDX[v] + 1 : FOFF[v];
-        s = nj;
-    } else {
-        u32 q = (u32)(i - A) >> 1;
-        if (((i - A) & 1) == 0) {
-            u32 r = ROOTS[q];
-            s = FOFF[r + 1] > FOFF[r] ? FOFF[r] : (u32)i + 1;
-        } else {
-            s = q + 1 < R ? A + 2 * (q + 1) : PG_INV;
+// Close every out-arc list into a cycle (a root's cycle exits through its up arc) and set
+// the virtual arcs: succ(2r) = NEXT[2r+1] = first out-arc of r (or 2r+1 if r is isolated);
+// succ(2r+1) = NEXT[2r] = down arc of the next root (or end of list).
+__global__ void k_arc_close(i64 n, const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
+                            const u32* __restrict__ P, const u32* __restrict__ RIDX,
+                            const u32* __restrict__ ROOTS, const Ctr* ctr, u32* NEXT) {
+    i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    uint2 e = HAB[x];
+    if (e.x != PG_INV) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            u32 arc = 2 * (u32)x + d;
+            if (NEXT[arc] == PG_INV) {          // tail of the list of its source vertex
+                u32 src = d == 0 ? e.x : e.y;
+                NEXT[arc] = P[src] == src ? 2 * src + 1 : HEAD[src];
+            }
         }
+    } else {
+        u32 r = (u32)x, h = HEAD[r];
+        NEXT[2 * r + 1] = h != PG_INV ? h : 2 * r + 1;
+        u32 q = RIDX[r] + 1;
+        NEXT[2 * r] = q < ctr->R ? 2 * ROOTS[q] : PG_INV;
     }
-    SUCC[i] = s;
 }
 
-__device__ __forceinline__ bool lr_is_ruler(u32 x, u32 head) { return (x & (LR_K - 1)) == 0 || x == head; }
-__device__ __forceinline__ u32 lr_ruler_index(u32 x, u32 nsk) { return (x & (LR_K - 1)) == 0 ? x / LR_K : nsk; }
+// root flags -> root index + root list (one fused scan)
+struct RootLoad {
+    const uint2* HAB;
+    __device__ __forceinline__ u32 operator()(i64 i) const { return HAB[i].x == PG_INV ? 1u : 0u; }
+};
+struct RootStore {
+    u32 *RIDX, *ROOTS;
+    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32 isroot) const {
+        RIDX[i] = ex;
+        if (isroot) ROOTS[ex] = (u32)i;
+    }
+};
 
-// ruler s walks its sublist: length and next ruler
-__global__ void k_lr_walk1(i64 L, i64 ns, const u32* __restrict__ SUCC, const u32* __restrict__ FOFF, i64 n,
-                           u32* SPLEN, u32* SPNEXT) {
+// ruling-set list ranking over succ(a) = NEXT[a^1]; rulers are the arcs a % LR_K == 0
+// (arc 0, the list head, is one).  walk1: length of each ruler's sublist and the next
+// ruler; Wyllie on the rulers; walk2: final positions + the tour payload per position.
+__global__ void k_lr_walk1(i64 ns, const u32* __restrict__ NEXT, u32* SPLEN, u32* SPNEXT) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    const u32 head = FOFF[n];
-    const u32 nsk = (u32)(ns - 1);
-    u32 e;
-    if (s < nsk) {
-        e = (u32)s * LR_K;
-    } else {
-        if ((head & (LR_K - 1)) == 0) { SPLEN[s] = 0; SPNEXT[s] = PG_INV; return; }
-        e = head;
-    }
-    u32 cnt = 0, x = e;
+    u32 cnt = 0, x = (u32)s * LR_K;
     do {
         ++cnt;
-        x = __ldg(SUCC + x);
-    } while (x != PG_INV && !lr_is_ruler(x, head));
+        x = __ldg(NEXT + (x ^ 1u));
+    } while (x != PG_INV && (x & (LR_K - 1)) != 0);
     SPLEN[s] = cnt;
-    SPNEXT[s] = x == PG_INV ? PG_INV : lr_ruler_index(x, nsk);
+    SPNEXT[s] = x == PG_INV ? PG_INV : x / LR_K;
 }
 
 // Wyllie pointer jumping on the rulers: suffix sums of sublist lengths
-__global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __restrict__ nxt_in, u32* len_out, u32* nxt_out) {
+__global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __restrict__ nxt_in, u32* len_out,
+                         u32* nxt_out) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     u32 nx = nxt_in[s];
@@ -324,48 +303,36 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
     nxt_out[s] = nx;
 }
 
-__global__ void k_lr_walk2(i64 L, i64 ns, const u32* __restrict__ SUCC, const u32* __restrict__ FOFF, i64 n,
-                           const u32* __restrict__ SUFFIX, u32* RANK) {
+// T[pos] = (twin arc << 32) | target vertex [| VFLAG for a root's down arc]
+__global__ void k_lr_walk2(i64 L, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
+                           const u32* __restrict__ SUFFIX, u32* RANK, u64* T) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    const u32 head = FOFF[n];
-    const u32 nsk = (u32)(ns - 1);
-    u32 e;
-    if (s < nsk) {
-        e = (u32)s * LR_K;
-    } else {
-        if ((head & (LR_K - 1)) == 0) return;
-        e = head;
-    }
-    u32 pos = (u32)L - SUFFIX[s], x = e;
+    u32 pos = (u32)L - SUFFIX[s], x = (u32)s * LR_K;
     do {
-        RANK[x] = pos++;
-        x = __ldg(SUCC + x);
-    } while (x != PG_INV && !lr_is_ruler(x, head));
+        RANK[x] = pos;
+        uint2 e = __ldg(HAB + (x >> 1));
+        u32 tg;
+        if (e.x != PG_INV) tg = (x & 1u) ? e.x : e.y;              // tree arc a->b / b->a
+        else tg = (x >> 1) | ((x & 1u) ? 0u : VFLAG);             // virtual arc of root x>>1
+        T[pos] = ((u64)(x ^ 1u) << 32) | tg;
+        ++pos;
+        x = __ldg(NEXT + (x ^ 1u));
+    } while (x != PG_INV && (x & (LR_K - 1)) != 0);
 }
 
-// T[rank(i)] = (rank(twin(i)) << 32) | target(i) [| VFLAG for a root's down arc]
-__global__ void k_tour_scatter(i64 n, const u32* __restrict__ FOFF, const u32* __restrict__ FADJ,
-                               const u32* __restrict__ FTWIN, const u32* __restrict__ ROOTS,
-                               const u32* __restrict__ RANK, u64* T) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 2 * n) return;
-    const u32 A = FOFF[n];
-    u32 tw, tg;
-    if (i < A) {
-        tw = FTWIN[i];
-        tg = FADJ[i];
-    } else {
-        tw = (u32)i ^ 1u;  // A is even
-        tg = ROOTS[(u32)(i - A) >> 1] | ((((u32)(i - A)) & 1u) == 0 ? VFLAG : 0u);
-    }
-    T[RANK[i]] = ((u64)RANK[tw] << 32) | tg;
-}
-
-// preorder pass (fused into a decoupled-look-back scan over tour positions)
+// preorder pass over tour positions, fused into a decoupled-look-back scan of the
+// "down arc" flags: an arc is down iff it precedes its twin.  The load resolves the twin's
+// position (one gather) and caches it in T's high word for the store.
 struct PreLoad {
-    const u64* T;
-    __device__ __forceinline__ u32 operator()(i64 k) const { return (u64)k < (T[k] >> 32) ? 1u : 0u; }
+    u64* T;
+    const u32* RANK;
+    __device__ __forceinline__ u32 operator()(i64 k) const {
+        u64 t = T[k];
+        u32 pt = RANK[(u32)(t >> 32)];
+        T[k] = ((u64)pt << 32) | (u32)t;
+        return (u64)k < pt ? 1u : 0u;
+    }
 };
 struct PreStore {
     const u64* T;
@@ -380,6 +347,7 @@ struct PreStore {
         u32 pt = (u32)(t >> 32), lo = (u32)t;
         u32 v = lo & ~VFLAG;
         u32 last = f + (pt - (u32)k + 1) / 2 - 1;
+        // the arc before a down arc u->v always ends at u
         u32 par = (lo & VFLAG) ? v : ((u32)T[k - 1] & ~VFLAG);
         FL[v] = make_uint2(f, last);
         FIRST[v] = f;
@@ -769,24 +737,6 @@ struct UoffStore {
     __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { UOFF[i] = ex; }
 };
 
-// deg scan -> forest offsets; root flags -> root index
-struct DegLoad {
-    const u32* FDEG;
-    __device__ __forceinline__ u32 operator()(i64 i) const { return FDEG[i]; }
-};
-struct OffStore {
-    u32* FOFF;
-    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { FOFF[i] = ex; }
-};
-struct RootLoad {
-    const u32* P;
-    __device__ __forceinline__ u32 operator()(i64 i) const { return P[i] == (u32)i ? 1u : 0u; }
-};
-struct RidxStore {
-    u32* RIDX;
-    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { RIDX[i] = ex; }
-};
-
 // --------------------------------------------------------------------------
 // validation (graph.py:87-107 ranges, graph.py:123-158 symmetry, SPEC.md:457 simple)
 // --------------------------------------------------------------------------
@@ -879,37 +829,34 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HA, w.C, w.ROOTMARK, w.FDEG, w.UCNT, w.CANON));
+    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C, w.ROOTMARK, w.UCNT, w.CANON));
     if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
-    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB));
+    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
-    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HA, w.HB, w.ctr, w.HEAVY));
-    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HA, w.HB, w.ctr, w.HEAVY));
+    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
+    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
-    // ---- S3 rooting
-    PG_K(k_forest_deg<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FDEG));
-    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), DegLoad{w.FDEG}, OffStore{w.FOFF}, w.FOFF + n, st));
-    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), RootLoad{w.P}, RidxStore{w.RIDX}, &w.ctr->R, st));
-    nl += 2;
-    PG_K(k_forest_fill<<<nblk(n, B), B, 0, st>>>(n, w.HA, w.HB, w.FOFF, w.FDEG, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS));
-    PG_K(k_succ<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.P, w.RIDX, w.ROOTS, w.ctr, w.SUCC));
+    // ---- S3 rooting: arc lists
+    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), RootLoad{w.HAB}, RootStore{w.RIDX, w.ROOTS}, &w.ctr->R, st));
+    ++nl;
+    PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    PG_K(k_arc_close<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.P, w.RIDX, w.ROOTS, w.ctr, w.NEXT));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
-    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[0], w.SPNEXT[0]));
+    // ---- S3 list ranking
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(w.ns, w.NEXT, w.SPLEN[0], w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
         PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.SUCC, w.FOFF, n, w.SPLEN[cur], w.RANK));
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.NEXT, w.HAB, w.SPLEN[cur], w.RANK, w.T));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
-    PG_K(k_tour_scatter<<<nblk(L, B), B, 0, st>>>(n, w.FOFF, w.FADJ, w.FTWIN, w.ROOTS, w.RANK, w.T));
-    PG_LAUNCH_CHECK();
-    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T},
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T, w.RANK},
                                  PreStore{w.T, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
