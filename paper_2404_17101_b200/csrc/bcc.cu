@@ -13,7 +13,7 @@
 // Stages (kernels), all stream-ordered, no host synchronisation:
 //   S2 First-CC   k_init, k_chunk_rows, k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
-//   S3 rooting    root scan, k_arc_link, k_arc_close, ruling-set list ranking (k_lr_walk1,
+//   S3 rooting    k_arc_link, root scan, k_arc_close, ruling-set list ranking (k_lr_walk1,
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
 //   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_cc2_sample, k_giant,
@@ -35,7 +35,8 @@ constexpr int GIANT_SAMPLES = 1024;
 constexpr int HEAVY_GRID = 148 * 4;
 
 struct Ctr {
-    u32 R;        // trees (roots) of the spanning forest
+    u64 roots;    // packed root-scan total: (non-isolated roots << 31) | isolated vertices
+    u32 R;        // trees (roots) of the spanning forest, isolated vertices included
     u32 giant;    // sampled largest component (First-CC)
     u32 giant2;   // sampled largest skeleton component (Last-CC)
     u32 ncomp;    // skeleton components
@@ -53,14 +54,15 @@ struct Ws {
     uint2* HAB;
     u32 *NEXT, *RANK;
     u32 *SPLEN[2], *SPNEXT[2];
-    u64* T;
+    u32* TA;      // arc at each tour position (walk2)
+    u64* T;       // (position of twin << 32) | target vertex [| VFLAG], per tour position
     uint2* FL;
     u32* FIRST;
     u32 *PV, *E, *PPAR;
     uint2 *W, *PM, *ST;
-    uint8_t* FEN;
-    u32* C;
-    uint2* FC;
+    u32* FPF;     // [position] parent's position | fence << 31 (PG_INV at roots)
+    u32* C;       // Last-CC union-find over preorder positions
+    u32* CIDV;    // per vertex: preorder rank of its skeleton component's head
     u32 *ROOTMARK, *UCNT, *UOFF, *CANON, *HEAVY;
     u32* CROW;
     u64* SCAN;
@@ -86,7 +88,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     i64 L = 2 * nn;
     w.nb = cdiv(nn, 32);
     w.lv = rmq_levels(w.nb);
-    w.ns = cdiv(L, LR_K);
+    w.ns = cdiv(L, LR_K) + 1;   // + the head ruler
     w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
@@ -100,6 +102,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
         w.SPLEN[b] = (u32*)take(4 * w.ns);
         w.SPNEXT[b] = (u32*)take(4 * w.ns);
     }
+    w.TA = (u32*)take(4 * L);
     w.T = (u64*)take(8 * L);
     w.FL = (uint2*)take(8 * nn);
     w.FIRST = (u32*)take(4 * nn);
@@ -109,9 +112,9 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.W = (uint2*)take(8 * nn);
     w.PM = (uint2*)take(8 * nn);
     w.ST = (uint2*)take(8 * w.nb * w.lv);
-    w.FEN = (uint8_t*)take(nn);
+    w.FPF = (u32*)take(4 * nn);
     w.C = (u32*)take(4 * nn);
-    w.FC = (uint2*)take(8 * nn);
+    w.CIDV = (u32*)take(4 * nn);
     w.ROOTMARK = (u32*)take(4 * nn);
     w.UCNT = (u32*)take(4 * nn);
     w.UOFF = (u32*)take(4 * nn);
@@ -206,8 +209,10 @@ __global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __re
 // virtual arcs: 2r = down into r, 2r+1 = up out of r.  Around every vertex the out-arcs
 // form a circular list NEXT (built with warp-aggregated atomicExch on HEAD[v]); the tour
 // successor is then uniformly succ(arc) = NEXT[arc^1].  A root's cycle is cut at its up
-// arc and consecutive roots are chained, so the forest is one list headed by arc 0
-// (vertex 0 is always a root: union by index keeps the minimum id as the root).
+// arc and consecutive non-isolated roots are chained, so the forest is one list headed by
+// the down arc of the first such root.  Isolated vertices (half of an RMAT graph) stay off
+// the tour: the root scan gives them preorder slots [0, NISO) directly, and the tour's
+// vertices take [NISO, n).
 // --------------------------------------------------------------------------
 
 // Insert `arc` at the head of key's circular out-arc list.  Lanes naming the same key
@@ -235,8 +240,10 @@ __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32*
 }
 
 // Close every out-arc list into a cycle (a root's cycle exits through its up arc) and set
-// the virtual arcs: succ(2r) = NEXT[2r+1] = first out-arc of r (or 2r+1 if r is isolated);
-// succ(2r+1) = NEXT[2r] = down arc of the next root (or end of list).
+// the virtual arcs of non-isolated roots: succ(2r) = NEXT[2r+1] = first out-arc of r;
+// succ(2r+1) = NEXT[2r] = down arc of the next non-isolated root (or end of list).
+constexpr u64 M31 = (1ull << 31) - 1;
+
 __global__ void k_arc_close(i64 n, const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
                             const u32* __restrict__ P, const u32* __restrict__ RIDX,
                             const u32* __restrict__ ROOTS, const Ctr* ctr, u32* NEXT) {
@@ -254,36 +261,96 @@ __global__ void k_arc_close(i64 n, const uint2* __restrict__ HAB, const u32* __r
         }
     } else {
         u32 r = (u32)x, h = HEAD[r];
-        NEXT[2 * r + 1] = h != PG_INV ? h : 2 * r + 1;
+        if (h == PG_INV) return;               // isolated vertex: not on the tour
+        NEXT[2 * r + 1] = h;
         u32 q = RIDX[r] + 1;
-        NEXT[2 * r] = q < ctr->R ? 2 * ROOTS[q] : PG_INV;
+        NEXT[2 * r] = q < (u32)(ctr->roots >> 31) ? 2 * ROOTS[q] : PG_INV;
     }
 }
 
-// root flags -> root index + root list (one fused scan)
+// Root scan over vertices, packed two-field sum: (non-isolated root << 31) | isolated.
+// Non-isolated roots get their chain index; isolated vertices get their preorder slot.
 struct RootLoad {
     const uint2* HAB;
-    __device__ __forceinline__ u32 operator()(i64 i) const { return HAB[i].x == PG_INV ? 1u : 0u; }
+    const u32* HEAD;   // PG_INV: no forest arcs (isolated, or only self-loops)
+    __device__ __forceinline__ u64 operator()(i64 v) const {
+        if (HAB[v].x != PG_INV) return 0;
+        return HEAD[v] == PG_INV ? 1ull : (1ull << 31);
+    }
 };
 struct RootStore {
     u32 *RIDX, *ROOTS;
-    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32 isroot) const {
-        RIDX[i] = ex;
-        if (isroot) ROOTS[ex] = (u32)i;
+    uint2* FL;
+    u32 *FIRST, *PV, *E, *PPAR;
+    uint2* W;
+    u32 *out_parent, *out_first;
+    __device__ __forceinline__ void operator()(i64 v, u64 ex, u64 val) const {
+        if (val >> 31) {
+            u32 k = (u32)(ex >> 31);
+            RIDX[v] = k;
+            ROOTS[k] = (u32)v;
+        } else if (val) {
+            u32 f = (u32)(ex & M31);
+            FL[v] = make_uint2(f, f);
+            FIRST[v] = f;
+            PV[f] = (u32)v;
+            E[f] = f;
+            PPAR[f] = (u32)v;
+            W[f] = make_uint2(f, f);
+            if (out_parent) out_parent[v] = (u32)v;
+            if (out_first) out_first[v] = f;
+        }
     }
 };
 
-// ruling-set list ranking over succ(a) = NEXT[a^1]; rulers are the arcs a % LR_K == 0
-// (arc 0, the list head, is one).  walk1: length of each ruler's sublist and the next
-// ruler; Wyllie on the rulers; walk2: final positions + the tour payload per position.
-__global__ void k_lr_walk1(i64 ns, const u32* __restrict__ NEXT, u32* SPLEN, u32* SPNEXT) {
+__global__ void k_roots_total(Ctr* ctr) {
+    u64 r = ctr->roots;
+    ctr->R = (u32)(r >> 31) + (u32)(r & M31);
+}
+
+// ruling-set list ranking over succ(a) = NEXT[a^1].  Rulers: every on-tour arc a with
+// a % LR_K == 0, plus the head (ruler index nsk).  walk1: each ruler's sublist length and
+// next ruler; Wyllie on the rulers; walk2: final positions (RANK) and TA[position] = arc.
+struct TourInfo {
+    u32 head;     // first arc of the list, PG_INV if the tour is empty
+    u32 len;      // arcs on the tour = 2 * (n - isolated)
+};
+__device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, const u32* ROOTS, i64 n) {
+    u64 r = ctr->roots;
+    TourInfo t;
+    t.head = (r >> 31) ? 2 * ROOTS[0] : PG_INV;
+    t.len = (u32)(2 * (n - (i64)(r & M31)));
+    return t;
+}
+__device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, const uint2* HAB, const u32* HEAD,
+                                            u32& x) {
+    if (s < nsk) {
+        x = (u32)s * LR_K;
+        u32 v = x >> 1;
+        return !(HAB[v].x == PG_INV && HEAD[v] == PG_INV);   // isolated vertices are off the tour
+    }
+    x = t.head;
+    return t.head != PG_INV && (t.head & (LR_K - 1)) != 0;
+}
+
+__global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
+                           const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr, u32* SPLEN,
+                           u32* SPNEXT) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    u32 cnt = 0, x = (u32)s * LR_K;
+    const TourInfo t = tour_info(ctr, ROOTS, n);
+    const i64 nsk = ns - 1;
+    u32 x;
+    if (!ruler_start(s, nsk, t, HAB, HEAD, x)) {
+        SPLEN[s] = 0;
+        SPNEXT[s] = PG_INV;
+        return;
+    }
+    u32 cnt = 0;
     do {
         ++cnt;
         x = __ldg(NEXT + (x ^ 1u));
-    } while (x != PG_INV && (x & (LR_K - 1)) != 0);
+    } while (x != PG_INV && (x & (LR_K - 1)) != 0);   // the head is never revisited
     SPLEN[s] = cnt;
     SPNEXT[s] = x == PG_INV ? PG_INV : x / LR_K;
 }
@@ -303,39 +370,47 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
     nxt_out[s] = nx;
 }
 
-// T[pos] = (twin arc << 32) | target vertex [| VFLAG for a root's down arc]
-__global__ void k_lr_walk2(i64 L, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
-                           const u32* __restrict__ SUFFIX, u32* RANK, u64* T) {
+__global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
+                           const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr,
+                           const u32* __restrict__ SUFFIX, u32* RANK, u32* TA) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    u32 pos = (u32)L - SUFFIX[s], x = (u32)s * LR_K;
+    const TourInfo t = tour_info(ctr, ROOTS, n);
+    u32 x;
+    if (!ruler_start(s, ns - 1, t, HAB, HEAD, x)) return;
+    u32 pos = t.len - SUFFIX[s];
     do {
+        u32 nx = __ldg(NEXT + (x ^ 1u));   // issue the chain load first
         RANK[x] = pos;
-        uint2 e = __ldg(HAB + (x >> 1));
-        u32 tg;
-        if (e.x != PG_INV) tg = (x & 1u) ? e.x : e.y;              // tree arc a->b / b->a
-        else tg = (x >> 1) | ((x & 1u) ? 0u : VFLAG);             // virtual arc of root x>>1
-        T[pos] = ((u64)(x ^ 1u) << 32) | tg;
+        TA[pos] = x;
         ++pos;
-        x = __ldg(NEXT + (x ^ 1u));
+        x = nx;
     } while (x != PG_INV && (x & (LR_K - 1)) != 0);
 }
 
 // preorder pass over tour positions, fused into a decoupled-look-back scan of the
-// "down arc" flags: an arc is down iff it precedes its twin.  The load resolves the twin's
-// position (one gather) and caches it in T's high word for the store.
+// "down arc" flags (an arc is down iff it precedes its twin).  The load resolves the
+// twin's position and the arc's target (two gathers) into T for the store.
 struct PreLoad {
-    u64* T;
+    const u32* TA;
     const u32* RANK;
+    const uint2* HAB;
+    u64* T;
+    const Ctr* ctr;
+    i64 n;
     __device__ __forceinline__ u32 operator()(i64 k) const {
-        u64 t = T[k];
-        u32 pt = RANK[(u32)(t >> 32)];
-        T[k] = ((u64)pt << 32) | (u32)t;
+        if (k >= 2 * (n - (i64)(ctr->roots & M31))) return 0u;
+        u32 x = TA[k];
+        u32 pt = RANK[x ^ 1u];
+        uint2 e = HAB[x >> 1];
+        u32 tg = e.x != PG_INV ? ((x & 1u) ? e.x : e.y) : ((x >> 1) | ((x & 1u) ? 0u : VFLAG));
+        T[k] = ((u64)pt << 32) | tg;
         return (u64)k < pt ? 1u : 0u;
     }
 };
 struct PreStore {
     const u64* T;
+    const Ctr* ctr;
     uint2* FL;
     u32* FIRST;
     u32 *PV, *E, *PPAR;
@@ -343,6 +418,7 @@ struct PreStore {
     u32 *out_parent, *out_first;
     __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
         if (!down) return;
+        f += (u32)(ctr->roots & M31);     // isolated vertices occupy [0, NISO)
         u64 t = T[k];
         u32 pt = (u32)(t >> 32), lo = (u32)t;
         u32 v = lo & ~VFLAG;
@@ -462,7 +538,7 @@ __global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i
 __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E,
                             const u32* __restrict__ PV, const u32* __restrict__ PPAR,
                             const uint2* __restrict__ PM, const uint2* __restrict__ ST, i64 nb,
-                            const uint2* __restrict__ FL, uint8_t* FEN /* [first] */, u32* C) {
+                            const uint2* __restrict__ FL, u32* FPF, u32* C) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool valid = i < n;
@@ -515,13 +591,14 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
         }
     }
     u32 v = PV[i], p = PPAR[i];
-    bool fence = false;
+    u32 fpf = PG_INV;
     if (p != v) {
         uint2 fp = FL[p];
-        fence = fp.x <= res.x && res.y <= fp.y;
-        if (!fence) uf_link(C, v, p);
+        bool fence = fp.x <= res.x && res.y <= fp.y;
+        if (!fence) uf_link(C, (u32)i, fp.x);   // Last-CC runs over preorder positions
+        fpf = fp.x | (fence ? 0x80000000u : 0u);
     }
-    FEN[i] = fence;  // preorder space: coalesced
+    FPF[i] = fpf;
 }
 
 // --------------------------------------------------------------------------
@@ -536,39 +613,45 @@ __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
     return !((fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y));
 }
 
+// Last-CC links preorder positions, so every skeleton component's union-find root is the
+// preorder rank of its head (the component's minimum).
 __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                              const uint2* __restrict__ FL, u32* C) {
     i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n) return;
     i64 a = off[u], b = off[u + 1];
-    if (a == b) return;
+    if (b - a < 2) return;     // a degree-1 vertex has only its tree edge
     if (b > a + SCAN2) b = a + SCAN2;
     uint2 fu = FL[u];
     int linked = 0;
     for (i64 s = a; s < b && linked < NSAMPLE2; ++s) {
-        u32 w = (u32)tgt[s];
-        if (is_cross(fu, FL[w])) {
-            uf_link(C, (u32)u, w);
+        uint2 fw = FL[(u32)tgt[s]];
+        if (is_cross(fu, fw)) {
+            uf_link(C, fu.x, fw.x);
             ++linked;
         }
     }
 }
 
-// tree roots have only back edges (every vertex of the tree descends from the root)
+// over preorder positions i (vertex PV[i]); tree roots have only back edges (every vertex
+// of the tree descends from the root), so they are skipped
 __global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                           const uint2* __restrict__ FL, const u32* __restrict__ P, u32* C, Ctr* ctr, u32* heavy) {
-    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
+                           const uint2* __restrict__ FL, const u32* __restrict__ PV, const u32* __restrict__ E,
+                           const u32* __restrict__ P, u32* C, Ctr* ctr, u32* heavy) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || ldcg(C + i) == ctr->giant2) return;
+    u32 u = PV[i];
+    if (P[u] == u) return;
     i64 a = off[u], b = off[u + 1];
-    if (a >= b || P[u] == (u32)u || ldcg(C + u) == ctr->giant2) return;
+    if (b - a < 2) return;
     if (b - a > HEAVY_ROW) {
-        heavy[atomicAdd(&ctr->nheavy2, 1u)] = (u32)u;
+        heavy[atomicAdd(&ctr->nheavy2, 1u)] = u;
         return;
     }
-    uint2 fu = FL[u];
+    uint2 fu = make_uint2((u32)i, E[i]);
     for (i64 s = a; s < b; ++s) {
-        u32 w = (u32)tgt[s];
-        if (is_cross(fu, FL[w])) uf_link(C, (u32)u, w);
+        uint2 fw = FL[(u32)tgt[s]];
+        if (is_cross(fu, fw)) uf_link(C, (u32)i, fw.x);
     }
 }
 
@@ -579,21 +662,23 @@ __global__ void k_cc2_rest_heavy(const i64* __restrict__ off, const int32_t* __r
         u32 u = heavy[h];
         uint2 fu = FL[u];
         for (i64 s = off[u] + threadIdx.x; s < off[u + 1]; s += blockDim.x) {
-            u32 w = (u32)tgt[s];
-            if (is_cross(fu, FL[w])) uf_link(C, u, w);
+            uint2 fw = FL[(u32)tgt[s]];
+            if (is_cross(fu, fw)) uf_link(C, fu.x, fw.x);
         }
     }
 }
 
-__global__ void k_compress_final(i64 n, u32* C, const uint2* __restrict__ FL, uint2* FC, Ctr* ctr, u32* out_comp) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+// final roots; CIDV[v] = preorder rank of the head of v's skeleton component
+__global__ void k_compress_final(i64 n, u32* C, const u32* __restrict__ PV, u32* CIDV, Ctr* ctr, u32* out_comp) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     u32 isroot = 0;
-    if (v < n) {
-        u32 c = uf_find(C, (u32)v);
-        stcg(C + v, c);
-        FC[v] = make_uint2(FL[v].x, c);
+    if (i < n) {
+        u32 c = uf_find(C, (u32)i);
+        stcg(C + i, c);
+        u32 v = PV[i];
+        CIDV[v] = c;
         if (out_comp) out_comp[v] = c;
-        isroot = c == (u32)v;
+        isroot = c == (u32)i;
     }
     u32 cnt = __popc(__ballot_sync(0xFFFFFFFFu, isroot));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr->ncomp, cnt);
@@ -606,31 +691,36 @@ __global__ void k_compress_final(i64 n, u32* C, const uint2* __restrict__ FL, ui
 // a fence and whose skeleton component differs from its parent's heads a BCC hanging off
 // the parent; a non-root parent is then an articulation point, a root only if its head
 // children span >= 2 components.  P (First-CC) has P[x] == x exactly at tree roots.
-__global__ void k_artic(i64 n, const u32* __restrict__ PV, const u32* __restrict__ PPAR,
-                        const uint8_t* __restrict__ FEN, const u32* __restrict__ C, const u32* __restrict__ P,
-                        u32* ROOTMARK, u32* bits) {
+__global__ void k_artic(i64 n, const u32* __restrict__ PPAR, const u32* __restrict__ FPF, const u32* __restrict__ C,
+                        const u32* __restrict__ P, u32* ROOTMARK, u32* bits) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || !FEN[i]) return;
-    u32 v = PV[i], p = PPAR[i];
-    u32 cv = C[v];
-    if (cv == C[p]) return;  // fence child inside p's own skeleton component: not a head
+    if (i >= n) return;
+    u32 f = FPF[i];
+    if (f == PG_INV || !(f & 0x80000000u)) return;
+    u32 ci = C[i];
+    if (ci == C[f & 0x7FFFFFFFu]) return;  // fence child inside p's own component: not a head
+    u32 p = PPAR[i];
     if (P[p] != p) {
         atomicOr(bits + (p >> 5), 1u << (p & 31));
     } else {
-        u32 old = atomicCAS(ROOTMARK + p, PG_INV, cv);
-        if (old != PG_INV && old != cv) atomicOr(bits + (p >> 5), 1u << (p & 31));
+        u32 old = atomicCAS(ROOTMARK + p, PG_INV, ci);
+        if (old != PG_INV && old != ci) atomicOr(bits + (p >> 5), 1u << (p & 31));
     }
 }
 
+// label(u,w) = component of the endpoint with the larger preorder rank (results.py:80-87).
+// With component ids = preorder rank of the component's head this is max(CID[u], CID[w]):
+// for a tree or back edge (a ancestor of d), either both share d's component or a is the
+// parent of d's component head, whose rank exceeds a's and hence a's component id; a
+// cross edge joins one component.  One 4-byte gather per slot.
 __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
-                                                      const uint2* __restrict__ FC, u32* label) {
+                                                      const u32* __restrict__ CIDV, u32* label) {
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
-    u32 w[WCH_U];
-    uint2 fw[WCH_U];
+    u32 w[WCH_U], cw[WCH_U];
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         i64 s = s0 + 32 * k + lane;
@@ -639,7 +729,7 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ of
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         i64 s = s0 + 32 * k + lane;
-        fw[k] = s < s1 ? __ldg(FC + w[k]) : make_uint2(0u, 0u);
+        cw[k] = s < s1 ? __ldg(CIDV + w[k]) : 0u;
     }
     u32 cur = crow[c];
 #pragma unroll
@@ -651,8 +741,8 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ of
         const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
         cur = __shfl_sync(0xFFFFFFFFu, row, 31);
         if (!valid) continue;
-        uint2 fu = __ldg(FC + row);
-        u32 lab = fu.x > fw[k].x ? fu.y : fw[k].y;
+        u32 cu = __ldg(CIDV + row);
+        u32 lab = cu > cw[k] ? cu : cw[k];
         if (w[k] == row) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
         __stcs(label + s, lab);
     }
@@ -840,24 +930,30 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
-    PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), RootLoad{w.HAB}, RootStore{w.RIDX, w.ROOTS}, &w.ctr->R, st));
-    ++nl;
     PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    PG_CUDA_TRY(launch_scan<u64>(n, w.SCAN, 0ull, SumOp(), RootLoad{w.HAB, w.HEAD},
+                                 RootStore{w.RIDX, w.ROOTS, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent,
+                                           out->first},
+                                 &w.ctr->roots, st));
+    PG_K(k_roots_total<<<1, 1, 0, st>>>(w.ctr));
+    ++nl;
     PG_K(k_arc_close<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.P, w.RIDX, w.ROOTS, w.ctr, w.NEXT));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
-    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(w.ns, w.NEXT, w.SPLEN[0], w.SPNEXT[0]));
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[0],
+                                                     w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
         PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(L, w.ns, w.NEXT, w.HAB, w.SPLEN[cur], w.RANK, w.T));
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[cur],
+                                                     w.RANK, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
-    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.T, w.RANK},
-                                 PreStore{w.T, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.RANK, w.HAB, w.T, w.ctr, n},
+                                 PreStore{w.T, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
@@ -868,23 +964,23 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
     for (i64 k = 1; k < w.lv; ++k)
         PG_K(k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb, (i64)1 << (k - 1)));
-    PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FEN, w.C));
+    PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FPF, w.C));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
     PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
-    PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.P, w.C, w.ctr, w.HEAVY));
+    PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
-    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FL, w.FC, w.ctr, out->comp));
+    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.PV, w.CIDV, w.ctr, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
     // ---- S6 articulation, labels, count
-    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PV, w.PPAR, w.FEN, w.C, w.P, w.ROOTMARK, out->artic_bits));
+    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FC, out->edge_label));
+    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));

@@ -65,6 +65,8 @@ def kats():
         # multigraph + self-loop: the reference pairs parallel edges by twin and leaves
         # self-loop slots unlabelled (-1)
         "multi_edge": Graph(*_multi()),
+        # vertex 1's only slot is a self-loop: it is isolated in the spanning forest
+        "selfloop_only": Graph(np.array([0, 1, 2, 3], dtype=np.int64), np.array([2, 1, 0], dtype=np.uint32)),
     }
     return cases
 
