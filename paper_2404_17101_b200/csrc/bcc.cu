@@ -20,7 +20,6 @@
 //                 k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
-#include <cstdlib>
 #include <cub/block/block_reduce.cuh>
 #include "common.cuh"
 #include "scan.cuh"
@@ -886,29 +885,6 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restr
 // --------------------------------------------------------------------------
 static inline unsigned nblk(i64 items, int bs) { return (unsigned)(items > 0 ? cdiv(items, bs) : 1); }
 
-// Experimental: keep the first `bytes` of a gathered per-vertex array L2-resident for the
-// per-slot gather passes (PASGAL_L2_HOT_MB; 0/unset = off).
-static size_t l2_hot_bytes() {
-    const char* e = getenv("PASGAL_L2_HOT_MB");
-    return e ? (size_t)atol(e) << 20 : 0;
-}
-static void l2_window(cudaStream_t st, const void* base, size_t bytes) {
-    cudaStreamAttrValue a = {};
-    if (bytes) {
-        static bool limit_set = false;
-        if (!limit_set) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
-            limit_set = true;
-        }
-        a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-        a.accessPolicyWindow.num_bytes = bytes;
-        a.accessPolicyWindow.hitRatio = 1.0f;
-        a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    }
-    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
-}
-
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr, size_t ws_bytes, u64 seed,
                u32 flags, cudaStream_t st, pasgal_bcc_prof_t* prof) {
     const i64 n = g->n, m = g->m_slots;
@@ -982,11 +958,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
-    const size_t hot = l2_hot_bytes() < 4 * (size_t)n ? l2_hot_bytes() : 4 * (size_t)n;
-    if (hot) l2_window(st, w.FIRST, hot);
     if (w.nch > 0) PG_K(k_tags<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
     PG_LAUNCH_CHECK();
-    if (hot) l2_window(st, nullptr, 0);
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
     for (i64 k = 1; k < w.lv; ++k)
@@ -1007,11 +980,9 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (hot) l2_window(st, w.CIDV, hot);
     if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
-    if (hot) l2_window(st, nullptr, 0);
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
     if (flags & PASGAL_BCC_CANONICAL) {
         if (w.nch > 0) PG_K(k_canon_count<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT));
