@@ -48,6 +48,26 @@ KERNEL_BYTES = {
 KERNEL_NAMES = {"tags": "k_tags", "labels": "k_labels"}
 
 
+def assign_instances(n_instances, rank, world):
+    """Config 5b: instances dealt round-robin to ranks (no data exchange between ranks)."""
+    return list(range(rank, n_instances, world))
+
+
+def reduce_over_ranks(total_ms, edges, device):
+    """Max of the device times and sum of the work over all ranks (timing plumbing only;
+    nothing on the data path is exchanged)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(total_ms), float(edges)
+    t = torch.tensor([float(total_ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e = torch.tensor([float(edges)], dtype=torch.float64, device=device)
+    dist.all_reduce(e, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(e.item())
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -281,15 +301,7 @@ def run_ours(args, rank, world, local):
         stage_ms[_lib.STAGES[si]] = statistics.mean(evs[k][si - 1].elapsed_time(evs[k][si]) for k in range(args.steps))
     total_ms = sum(step_ms)
     window_ms = win0.elapsed_time(win1)
-    edges = mu * args.steps
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e = torch.tensor([edges], dtype=torch.float64, device=dev)
-        dist.all_reduce(e, op=dist.ReduceOp.SUM)
-        total_ms, edges = float(t.item()), float(e.item())
+    total_ms, edges = reduce_over_ranks(total_ms, mu * args.steps, dev)
     value = edges / (total_ms / 1e3)
 
     peak, peak_src = measured_peak()
@@ -348,6 +360,73 @@ def run_ours(args, rank, world, local):
     return 0
 
 
+def run_batch(args, rank, world, local):
+    """Config 5b: a batch of `--instances` independent 4096x4096 p=0.6 grids (seeds 1..64),
+    dealt round-robin to the ranks, each generated on its GPU and kept resident; one step =
+    FAST-BCC over all of the rank's instances.  Reports edges/s and instances/s."""
+    import torch
+
+    import paper_2404_17101_b200 as pg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    mine = assign_instances(args.instances, rank, world)
+    graphs = [pg.gen_grid(4096, 4096, 0.6, 1 + i, device=dev) for i in mine]
+    torch.cuda.synchronize()
+    nmax = max((g.n for g in graphs), default=1)
+    mmax = max((g.m for g in graphs), default=1)
+    ws = torch.empty(pg.workspace_bytes(nmax, mmax), dtype=torch.uint8, device=dev)
+    out = pg.DeviceBcc(edge_label=torch.empty(mmax, dtype=torch.int32, device=dev),
+                       artic_bits=torch.empty((nmax + 31) // 32, dtype=torch.int32, device=dev),
+                       bcc_count=torch.empty(1, dtype=torch.int64, device=dev))
+    launches = 0
+
+    def step():
+        nl = 0
+        for g in graphs:
+            nl += pg.bcc_device(g.offsets, g.targets, out=out, workspace=ws).launches
+        return nl
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        launches += step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    total_ms = e0.elapsed_time(e1)
+    mu = sum(g.m // 2 for g in graphs) * args.steps
+    total_ms, edges = reduce_over_ranks(total_ms, mu, dev)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": edges / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": f"c5b: batch of {args.instances} grid 4096x4096 p=0.6 instances, seeds 1..{args.instances}",
+                       "instances_per_s": args.instances * args.steps / (total_ms / 1e3),
+                       "l2": "inputs larger than L2 (batch of 64 x 295 MB CSR)"},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def run_e2e(args, dg, dev, n, m):
     """The same metric through pg.bcc(g): H2D of the CSR from pinned host memory, device
     validation (the reference's is_symmetric), FAST-BCC, D2H of labels + articulation bitmap
@@ -384,7 +463,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c5a", choices=["c1", "c2", "c3", "c4", "c5a"])
+    ap.add_argument("--config", default="c5a", choices=["c1", "c2", "c3", "c4", "c5a", "c5b"])
+    ap.add_argument("--instances", type=int, default=64, help="c5b: batch size (grid instances)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0, help="sampling seed of the BCC call")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -394,6 +474,8 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.config == "c5b":
+        return run_batch(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 

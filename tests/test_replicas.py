@@ -1,0 +1,58 @@
+"""CPU: the multi-GPU plumbing of bench.py (replicas only -- BCC of one graph does not
+shard) on a world-size-2 gloo group: instance dealing for config 5b
+and the max-time / summed-work reduction the whole-job value is built from."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+
+    mine = bench.assign_instances(64, rank, world)
+    t, e = bench.reduce_over_ranks(10.0 + 5 * rank, 1000 * (rank + 1), "cpu")
+    q.put((rank, mine, t, e))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_reduction_and_dealing():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+    (r0, m0, t0, e0), (r1, m1, t1, e1) = res
+    assert sorted(m0 + m1) == list(range(64)) and not set(m0) & set(m1)
+    assert len(m0) == len(m1) == 32
+    assert t0 == t1 == 15.0           # max over ranks
+    assert e0 == e1 == 3000.0         # whole-job work
+
+
+def test_single_process_passthrough():
+    import bench
+
+    assert bench.reduce_over_ranks(7.5, 42, "cpu") == (7.5, 42.0)
+    assert bench.assign_instances(5, 0, 1) == [0, 1, 2, 3, 4]
