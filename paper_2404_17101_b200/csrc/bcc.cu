@@ -43,7 +43,7 @@ struct Ctr {
     u32 verr;     // validation error bits
     u32 nheavy;   // heavy rows queued by k_cc_rest
     u32 nheavy2;  // heavy rows queued by k_cc2_rest
-    u32 pad;
+    u32 gcid;     // component id (head preorder rank) of the sampled giant skeleton component
 };
 
 // --------------------------------------------------------------------------
@@ -63,6 +63,7 @@ struct Ws {
     u32* FPF;     // [position] parent's position | fence << 31 (PG_INV at roots)
     u32* C;       // Last-CC union-find over preorder positions
     u32* CIDV;    // per vertex: preorder rank of its skeleton component's head
+    u32* GBIT;    // per vertex bit: CIDV[v] == gcid (33 MB at 2^28: L2-resident)
     u32 *ROOTMARK, *UCNT, *UOFF, *CANON, *HEAVY;
     u32* CROW;
     u64* SCAN;
@@ -115,6 +116,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.FPF = (u32*)take(4 * nn);
     w.C = (u32*)take(4 * nn);
     w.CIDV = (u32*)take(4 * nn);
+    w.GBIT = (u32*)take(4 * w.nb);
     w.ROOTMARK = (u32*)take(4 * nn);
     w.UCNT = (u32*)take(4 * nn);
     w.UOFF = (u32*)take(4 * nn);
@@ -708,18 +710,32 @@ __global__ void k_artic(i64 n, const u32* __restrict__ PPAR, const u32* __restri
     }
 }
 
+// the giant skeleton component's final id and its membership bitmap (one ballot per word)
+__global__ void k_giant_bits(i64 n, const u32* __restrict__ C, const u32* __restrict__ CIDV, Ctr* ctr, u32* GBIT) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 g = C[ctr->giant2];        // C is fully compressed: the root of the sampled giant
+    if (v == 0) ctr->gcid = g;
+    bool in = v < n && CIDV[v] == g;
+    unsigned b = __ballot_sync(0xFFFFFFFFu, in);
+    if ((threadIdx.x & 31) == 0 && v < n) GBIT[v >> 5] = b;
+}
+
 // label(u,w) = component of the endpoint with the larger preorder rank (results.py:80-87).
 // With component ids = preorder rank of the component's head this is max(CID[u], CID[w]):
 // for a tree or back edge (a ancestor of d), either both share d's component or a is the
 // parent of d's component head, whose rank exceeds a's and hence a's component id; a
-// cross edge joins one component.  One 4-byte gather per slot.
+// cross edge joins one component.  Most slots of a power-law graph point into the giant
+// component, so the target's component comes from the L2-resident membership bitmap and
+// only the remaining slots gather CIDV from HBM.
 __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
-                                                      const u32* __restrict__ CIDV, u32* label) {
+                                                      const u32* __restrict__ CIDV, const u32* __restrict__ GBIT,
+                                                      const Ctr* __restrict__ ctr, u32* label) {
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    const u32 g = ctr->gcid;
     u32 w[WCH_U], cw[WCH_U];
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
@@ -729,7 +745,12 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ of
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         i64 s = s0 + 32 * k + lane;
-        cw[k] = s < s1 ? __ldg(CIDV + w[k]) : 0u;
+        cw[k] = s < s1 ? __ldg(GBIT + (w[k] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) {
+        i64 s = s0 + 32 * k + lane;
+        cw[k] = (cw[k] >> (w[k] & 31)) & 1u ? g : (s < s1 ? __ldg(CIDV + w[k]) : 0u);
     }
     u32 cur = crow[c];
 #pragma unroll
@@ -974,13 +995,15 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
     PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.PV, w.CIDV, w.ctr, out->comp));
+    PG_K(k_giant_bits<<<nblk(n, B), B, 0, st>>>(n, w.C, w.CIDV, w.ctr, w.GBIT));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
     // ---- S6 articulation, labels, count
     PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, out->edge_label));
+    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, w.GBIT, w.ctr,
+                                                                          out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
