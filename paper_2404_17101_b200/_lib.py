@@ -10,7 +10,7 @@ import os
 
 from . import _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("PASGAL_BCC_LIB", _build.LIB)   # override: experiment variants
 
 PASGAL_OK = 0
 PASGAL_EINVAL = 1

@@ -608,8 +608,14 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 // NSAMPLE2 cross edges among its first SCAN2 slots, so the big skeleton component forms
 // before the sampled-giant rows are skipped by the full pass.
 // --------------------------------------------------------------------------
-constexpr int NSAMPLE2 = 2;
-constexpr int SCAN2 = 6;
+#ifndef PG_NSAMPLE2
+#define PG_NSAMPLE2 2
+#endif
+#ifndef PG_SCAN2
+#define PG_SCAN2 6
+#endif
+constexpr int NSAMPLE2 = PG_NSAMPLE2;
+constexpr int SCAN2 = PG_SCAN2;
 
 __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
     return !((fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y));

@@ -17,7 +17,10 @@
 
 namespace pg {
 
-constexpr int WCH_U = 8;
+#ifndef PG_WCH_U
+#define PG_WCH_U 8
+#endif
+constexpr int WCH_U = PG_WCH_U;
 constexpr int WCH = 32 * WCH_U;   // slots per warp chunk
 constexpr int WCH_BLOCK = 256;    // threads per block (8 warps = 8 chunks)
 
