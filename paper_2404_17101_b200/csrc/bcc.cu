@@ -609,10 +609,10 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 // before the sampled-giant rows are skipped by the full pass.
 // --------------------------------------------------------------------------
 #ifndef PG_NSAMPLE2
-#define PG_NSAMPLE2 2
+#define PG_NSAMPLE2 1
 #endif
 #ifndef PG_SCAN2
-#define PG_SCAN2 6
+#define PG_SCAN2 4
 #endif
 constexpr int NSAMPLE2 = PG_NSAMPLE2;
 constexpr int SCAN2 = PG_SCAN2;
