@@ -11,13 +11,14 @@
 //     (a fence child can share p's skeleton component through a cross edge).
 //
 // Stages (kernels), all stream-ordered, no host synchronisation:
-//   S2 First-CC   k_init, k_chunk_rows, k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
+//   S2 First-CC   k_init, k_chunk_rows, k_cc_local (shared-memory union-find per id block),
+//                 k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
 //   S3 rooting    k_arc_link, root scan, k_arc_close, ruling-set list ranking (k_lr_walk1,
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
-//   S5 Last-CC    fused into k_rmq_query (non-fence tree edges), k_cc2_sample, k_giant,
-//                 k_cc2_rest(+heavy)
+//   S5 Last-CC    k_cc2_local / k_cc2_tree (non-fence tree edges, preorder blocks in shared
+//                 memory first), k_cc2_sample, k_giant, k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
 #include <cub/block/block_reduce.cuh>
@@ -132,23 +133,83 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
 // S2: First-CC (spanning forest by union-find with hook capture; Afforest-style
 // neighbour sampling, then skip the sampled giant component)
 // --------------------------------------------------------------------------
-__global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C, u32* ROOTMARK, u32* UCNT, u32* CANON) {
+__global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     P[v] = (u32)v;
     C[v] = (u32)v;
     HAB[v] = make_uint2(PG_INV, PG_INV);
     HEAD[v] = PG_INV;
-    ROOTMARK[v] = PG_INV;
+}
+
+__global__ void k_canon_init(i64 n, u32* UCNT, u32* CANON) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
     UCNT[v] = 0;
     CANON[v] = PG_INV;
 }
 
+// Local phase (the paper's vertical granularity control recast for the GPU): a CTA owns a
+// block of LOCAL_B consecutive ids and runs union-find on the block's internal sampled
+// edges in shared memory, then publishes flat parents P[v] = block root.  Chains along the
+// block (grid rows, preorder paths) collapse at shared-memory latency instead of walking
+// global memory; only block-crossing edges reach the global union-find.
+constexpr int LOCAL_LB = 12;
+constexpr int LOCAL_B = 1 << LOCAL_LB;
+constexpr int LOCAL_T = 512;
+
+__device__ __forceinline__ u32 sfind(volatile u32* sp, u32 x) {
+    for (;;) {
+        u32 p = sp[x];
+        if (p == x) return x;
+        u32 gp = sp[p];
+        if (gp == p) return p;
+        sp[x] = gp;
+        x = gp;
+    }
+}
+
+// link local ids a-b; returns the hooked local root (or PG_INV if already joined)
+__device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
+    u32 ra = sfind(sp, a), rb = sfind(sp, b);
+    while (ra != rb) {
+        u32 hi = ra > rb ? ra : rb, lo = ra ^ rb ^ hi;
+        if (atomicCAS(sp + hi, hi, lo) == hi) return hi;
+        ra = sfind(sp, ra);
+        rb = sfind(sp, rb);
+    }
+    return PG_INV;
+}
+
+__global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restrict__ off,
+                                                      const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
+    __shared__ u32 sp[LOCAL_B];
+    const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
+    const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) sp[i] = (u32)i;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
+        i64 v = b0 + i, a = off[v], b = off[v + 1];
+        for (int k = 0; k < NSAMPLE && a + k < b; ++k) {
+            i64 w = tgt[a + k];
+            if ((w >> LOCAL_LB) != blockIdx.x) continue;
+            u32 hi = slink(sp, (u32)i, (u32)(w - b0));
+            if (hi != PG_INV) HAB[b0 + hi] = make_uint2((u32)v, (u32)w);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) P[b0 + i] = (u32)b0 + sfind(sp, (u32)i);
+}
+
+// sampled edges that cross blocks (the local phase took the rest)
 __global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     i64 a = off[v], b = off[v + 1];
-    for (int k = 0; k < NSAMPLE && a + k < b; ++k) uf_link_hook(P, (u32)v, (u32)tgt[a + k], HAB);
+    for (int k = 0; k < NSAMPLE && a + k < b; ++k) {
+        u32 w = (u32)tgt[a + k];
+        if ((w >> LOCAL_LB) != (u32)(v >> LOCAL_LB)) uf_link_hook(P, (u32)v, w, HAB);
+    }
 }
 
 __global__ void k_compress(i64 n, u32* P) {
@@ -281,7 +342,7 @@ struct RootLoad {
     }
 };
 struct RootStore {
-    u32 *RIDX, *ROOTS;
+    u32 *RIDX, *ROOTS, *ROOTMARK;
     uint2* FL;
     u32 *FIRST, *PV, *E, *PPAR;
     uint2* W;
@@ -291,6 +352,7 @@ struct RootStore {
             u32 k = (u32)(ex >> 31);
             RIDX[v] = k;
             ROOTS[k] = (u32)v;
+            ROOTMARK[v] = PG_INV;          // root articulation marker (k_artic)
         } else if (val) {
             u32 f = (u32)(ex & M31);
             FL[v] = make_uint2(f, f);
@@ -597,8 +659,7 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
     if (p != v) {
         uint2 fp = FL[p];
         bool fence = fp.x <= res.x && res.y <= fp.y;
-        if (!fence) uf_link(C, (u32)i, fp.x);   // Last-CC runs over preorder positions
-        fpf = fp.x | (fence ? 0x80000000u : 0u);
+        fpf = fp.x | (fence ? 0x80000000u : 0u);  // non-fence tree edges: k_cc2_local / _tree
     }
     FPF[i] = fpf;
 }
@@ -623,6 +684,33 @@ __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
 
 // Last-CC links preorder positions, so every skeleton component's union-find root is the
 // preorder rank of its head (the component's minimum).
+// Last-CC local phase over preorder positions: non-fence tree edges (i, parent position)
+// inside a block of LOCAL_B positions are joined in shared memory (a child's parent is
+// usually a few positions back), then C[i] = block root is published.
+__global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restrict__ FPF, u32* C) {
+    __shared__ u32 sp[LOCAL_B];
+    const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
+    const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) sp[i] = (u32)i;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
+        u32 f = FPF[b0 + i];
+        if (f & 0x80000000u) continue;     // fence, or a root (PG_INV)
+        if ((i64)f >= b0) slink(sp, (u32)i, (u32)(f - b0));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) C[b0 + i] = (u32)b0 + sfind(sp, (u32)i);
+}
+
+// non-fence tree edges whose parent lies in an earlier block
+__global__ void k_cc2_tree(i64 n, const u32* __restrict__ FPF, u32* C) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    u32 f = FPF[i];
+    if (f & 0x80000000u) return;
+    if ((f >> LOCAL_LB) != (u32)(i >> LOCAL_LB)) uf_link(C, (u32)i, f);
+}
+
 __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                              const uint2* __restrict__ FL, u32* C) {
     i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -946,20 +1034,21 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C, w.ROOTMARK, w.UCNT, w.CANON));
+    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C));
     if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
     PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
-    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
+    // no final compress: later stages only ask "is x a root", and P[x] == x exactly at roots
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
     PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
     PG_CUDA_TRY(launch_scan<u64>(n, w.SCAN, 0ull, SumOp(), RootLoad{w.HAB, w.HEAD},
-                                 RootStore{w.RIDX, w.ROOTS, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent,
+                                 RootStore{w.RIDX, w.ROOTS, w.ROOTMARK, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent,
                                            out->first},
                                  &w.ctr->roots, st));
     PG_K(k_roots_total<<<1, 1, 0, st>>>(w.ctr));
@@ -995,6 +1084,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
+    PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.C));
+    PG_K(k_cc2_tree<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.C));
     PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
     PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
@@ -1014,6 +1105,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
     if (flags & PASGAL_BCC_CANONICAL) {
+        PG_K(k_canon_init<<<nblk(n, B), B, 0, st>>>(n, w.UCNT, w.CANON));
         if (w.nch > 0) PG_K(k_canon_count<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT));
         PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), UcntLoad{w.UCNT}, UoffStore{w.UOFF}, (u32*)nullptr, st));
         ++nl;
