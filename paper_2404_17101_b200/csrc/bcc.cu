@@ -21,6 +21,8 @@
 //                 memory first), k_cc2_sample, k_giant, k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
+#include <cstdio>
+#include <cstdlib>
 #include <cub/block/block_reduce.cuh>
 #include "common.cuh"
 #include "scan.cuh"
@@ -1017,10 +1019,20 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
             return cudaEventRecord((cudaEvent_t)prof->events[stage], st);
         return cudaSuccess;
     };
-#define PG_K(...)        \
-    do {                 \
-        __VA_ARGS__;     \
-        ++nl;            \
+    static const bool debug = getenv("PASGAL_BCC_DEBUG") != nullptr;
+#define PG_K(...)                                                                          \
+    do {                                                                                   \
+        __VA_ARGS__;                                                                       \
+        ++nl;                                                                              \
+        if (debug) {                                                                       \
+            cudaError_t e_ = cudaStreamSynchronize(st);                                    \
+            if (e_ == cudaSuccess) e_ = cudaGetLastError();                                \
+            if (e_ != cudaSuccess) {                                                       \
+                fprintf(stderr, "pasgal_bcc: launch %d (%s) failed: %s\n", nl, #__VA_ARGS__, \
+                        cudaGetErrorString(e_));                                           \
+                return PASGAL_ECUDA;                                                       \
+            }                                                                              \
+        }                                                                                  \
     } while (0)
 
     PG_CUDA_TRY(mark(PASGAL_STAGE_BEGIN));
