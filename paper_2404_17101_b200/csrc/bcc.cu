@@ -456,9 +456,11 @@ __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
 
 // preorder pass over tour positions, fused into a decoupled-look-back scan of the
 // "down arc" flags (an arc is down iff it precedes its twin).  The load resolves the
-// twin's position and the arc's target (two gathers) into T for the store.
+// twin's position, the arc's target and its source (the parent, for a down arc) and
+// stashes them in this tile's own T[k] / TA[k]: the store must not read another tile's
+// items, which the look-back does not order.
 struct PreLoad {
-    const u32* TA;
+    u32* TA;
     const u32* RANK;
     const uint2* HAB;
     u64* T;
@@ -469,13 +471,22 @@ struct PreLoad {
         u32 x = TA[k];
         u32 pt = RANK[x ^ 1u];
         uint2 e = HAB[x >> 1];
-        u32 tg = e.x != PG_INV ? ((x & 1u) ? e.x : e.y) : ((x >> 1) | ((x & 1u) ? 0u : VFLAG));
+        u32 tg, src;
+        if (e.x != PG_INV) {                 // tree arc 2y = a->b, 2y+1 = b->a
+            tg = (x & 1u) ? e.x : e.y;
+            src = (x & 1u) ? e.y : e.x;
+        } else {                             // virtual arc of root y: parent = self
+            tg = (x >> 1) | ((x & 1u) ? 0u : VFLAG);
+            src = x >> 1;
+        }
         T[k] = ((u64)pt << 32) | tg;
+        TA[k] = src;
         return (u64)k < pt ? 1u : 0u;
     }
 };
 struct PreStore {
     const u64* T;
+    const u32* TA;
     const Ctr* ctr;
     uint2* FL;
     u32* FIRST;
@@ -489,8 +500,8 @@ struct PreStore {
         u32 pt = (u32)(t >> 32), lo = (u32)t;
         u32 v = lo & ~VFLAG;
         u32 last = f + (pt - (u32)k + 1) / 2 - 1;
-        // the arc before a down arc u->v always ends at u
-        u32 par = (lo & VFLAG) ? v : ((u32)T[k - 1] & ~VFLAG);
+        u32 par = TA[k];                 // source of the down arc p->v
+        (void)lo;
         FL[v] = make_uint2(f, last);
         FIRST[v] = f;
         PV[f] = v;
@@ -1081,7 +1092,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.RANK, w.HAB, w.T, w.ctr, n},
-                                 PreStore{w.T, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+                                 PreStore{w.T, w.TA, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
