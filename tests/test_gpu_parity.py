@@ -203,3 +203,24 @@ def test_large_diameter_chain_and_grid():
     assert cnt == n - 1
     dg = pg.gen_grid(2000, 2000, 1.0, 0)
     assert _parity_device_graph(dg) == 1
+
+
+def test_repeated_calls_reuse_workspace():
+    """Back-to-back calls on one cached workspace stay bit-exact.  Stale data from the
+    previous call must never leak into the next: every call re-derives its union-find
+    forest (schedule-dependent), so a read that crosses a scan tile without ordering shows
+    up here as wrong parents (regression test for the preorder-scan store)."""
+    dg = pg.gen_rmat(18, 8 << 18, seed=11)
+    off = dg.offsets.cpu().numpy()
+    tgt = dg.targets.cpu().numpy().view(np.uint32)
+    ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+    want = oracle.canonical_min_eid(off, tgt, ref.edge_label)
+    for it in range(6):
+        r = pg.bcc_device(dg.offsets, dg.targets, seed=it, canonical=(it % 2 == 0))
+        lab, art, cnt = _host_out(r, dg.n)
+        assert cnt == ref.bcc_count and np.array_equal(art, ref.articulation), it
+        if it % 2 == 0:
+            assert np.array_equal(lab, want), it
+        else:
+            got = pg.canonical_edge_partition(pg.Graph(off, tgt), pg.BccLabels(art, cnt, edge_label=lab))
+            assert np.array_equal(got, pg.min_eid_to_partition(pg.Graph(off, tgt), want)), it
