@@ -58,6 +58,7 @@ struct Ws {
     u32 *NEXT, *RANK;
     u32 *SPLEN[2], *SPNEXT[2];
     u32* TA;      // arc at each tour position (walk2)
+    u32* TP;      // parent (source vertex) of the arc at each tour position
     u64* T;       // (position of twin << 32) | target vertex [| VFLAG], per tour position
     uint2* FL;
     u32* FIRST;
@@ -107,6 +108,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
         w.SPNEXT[b] = (u32*)take(4 * w.ns);
     }
     w.TA = (u32*)take(4 * L);
+    w.TP = (u32*)take(4 * L);
     w.T = (u64*)take(8 * L);
     w.FL = (uint2*)take(8 * nn);
     w.FIRST = (u32*)take(4 * nn);
@@ -280,28 +282,44 @@ __global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __re
 // vertices take [NISO, n).
 // --------------------------------------------------------------------------
 
-// Insert `arc` at the head of key's circular out-arc list.  Lanes naming the same key
-// (hubs) are chained locally and spliced in with one atomicExch.
-__device__ __forceinline__ void arc_push(u32* HEAD, u32* NEXT, u32 key, u32 arc, bool active) {
+// Insert arcs at the heads of their keys' circular out-arc lists.  Lanes naming the same
+// key (hubs) are chained locally and spliced in with one atomicExch; each thread pushes
+// its two arcs with both exchanges in flight before either result is used.
+struct ArcGroup {
+    unsigned grp;
+    int lead;
+    unsigned later;
+};
+__device__ __forceinline__ ArcGroup arc_group(u32 key, bool active, int lane) {
+    ArcGroup g{0u, 0, 0u};
     unsigned act = __ballot_sync(0xFFFFFFFFu, active);
-    if (!active) return;
-    const int lane = threadIdx.x & 31;
-    unsigned grp = __match_any_sync(act, key);
-    int lead = __ffs(grp) - 1;
-    u32 old = 0;
-    if (lane == lead) old = atomicExch(HEAD + key, arc);
-    old = __shfl_sync(grp, old, lead);
-    unsigned later = grp & (lane == 31 ? 0u : (0xFFFFFFFEu << lane));
-    u32 nxt_arc = __shfl_sync(grp, arc, later ? __ffs(later) - 1 : lane);
-    NEXT[arc] = later ? nxt_arc : old;   // the group's last arc continues into the old list
+    if (active) {
+        g.grp = __match_any_sync(act, key);
+        g.lead = __ffs(g.grp) - 1;
+        g.later = g.grp & (lane == 31 ? 0u : (0xFFFFFFFEu << lane));
+    }
+    return g;
+}
+__device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc, u32 old) {
+    old = __shfl_sync(g.grp, old, g.lead);
+    u32 nxt = __shfl_sync(g.grp, arc, g.later ? __ffs(g.later) - 1 : (threadIdx.x & 31));
+    NEXT[arc] = g.later ? nxt : old;   // the group's last arc continues into the old list
 }
 
 __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
     i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     uint2 e = x < n ? HAB[x] : make_uint2(PG_INV, PG_INV);
-    bool act = e.x != PG_INV;
-    arc_push(HEAD, NEXT, e.x, 2 * (u32)x, act);       // a -> b is an out-arc of a
-    arc_push(HEAD, NEXT, e.y, 2 * (u32)x + 1, act);   // b -> a is an out-arc of b
+    const bool act = e.x != PG_INV;
+    const u32 arc_a = 2 * (u32)x, arc_b = 2 * (u32)x + 1;   // a->b out of a, b->a out of b
+    ArcGroup ga = arc_group(e.x, act, lane);
+    ArcGroup gb = arc_group(e.y, act, lane);
+    if (!act) return;
+    u32 olda = 0, oldb = 0;
+    if (lane == ga.lead) olda = atomicExch(HEAD + e.x, arc_a);
+    if (lane == gb.lead) oldb = atomicExch(HEAD + e.y, arc_b);
+    arc_splice(NEXT, ga, arc_a, olda);
+    arc_splice(NEXT, gb, arc_b, oldb);
 }
 
 // Close every out-arc list into a cycle (a root's cycle exits through its up arc) and set
@@ -460,17 +478,20 @@ __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
 // stashes them in this tile's own T[k] / TA[k]: the store must not read another tile's
 // items, which the look-back does not order.
 struct PreLoad {
-    u32* TA;
+    const u32* TA;
     const u32* RANK;
     const uint2* HAB;
     u64* T;
+    u32* TP;
     const Ctr* ctr;
     i64 n;
+    // all reads are read-only for the kernel (__ldg), so the compiler may issue the next
+    // items' gathers before this item's stores
     __device__ __forceinline__ u32 operator()(i64 k) const {
         if (k >= 2 * (n - (i64)(ctr->roots & M31))) return 0u;
-        u32 x = TA[k];
-        u32 pt = RANK[x ^ 1u];
-        uint2 e = HAB[x >> 1];
+        u32 x = __ldg(TA + k);
+        u32 pt = __ldg(RANK + (x ^ 1u));
+        uint2 e = __ldg(HAB + (x >> 1));
         u32 tg, src;
         if (e.x != PG_INV) {                 // tree arc 2y = a->b, 2y+1 = b->a
             tg = (x & 1u) ? e.x : e.y;
@@ -480,13 +501,13 @@ struct PreLoad {
             src = x >> 1;
         }
         T[k] = ((u64)pt << 32) | tg;
-        TA[k] = src;
+        TP[k] = src;
         return (u64)k < pt ? 1u : 0u;
     }
 };
 struct PreStore {
     const u64* T;
-    const u32* TA;
+    const u32* TP;
     const Ctr* ctr;
     uint2* FL;
     u32* FIRST;
@@ -500,7 +521,7 @@ struct PreStore {
         u32 pt = (u32)(t >> 32), lo = (u32)t;
         u32 v = lo & ~VFLAG;
         u32 last = f + (pt - (u32)k + 1) / 2 - 1;
-        u32 par = TA[k];                 // source of the down arc p->v
+        u32 par = TP[k];                 // source of the down arc p->v
         (void)lo;
         FL[v] = make_uint2(f, last);
         FIRST[v] = f;
@@ -1091,8 +1112,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
                                                      w.RANK, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
-    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.RANK, w.HAB, w.T, w.ctr, n},
-                                 PreStore{w.T, w.TA, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.RANK, w.HAB, w.T, w.TP, w.ctr, n},
+                                 PreStore{w.T, w.TP, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));

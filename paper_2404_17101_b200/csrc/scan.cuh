@@ -5,8 +5,11 @@
 // the look-back spin).  Each tile publishes a 64-bit status word: flag in bits 62-63
 // (0 = empty, 1 = tile aggregate, 2 = inclusive prefix) and the value in bits 0-61, so
 // flag and value land in one single-copy-atomic store and need no fence.  Values must
-// fit in 62 bits.  Load and store are functors, so a scan can be fused with its
-// producer (load) and consumer (store) -- e.g. the preorder pass of the rooting stage.
+// fit in 62 bits.  The look-back is warp-parallel: warp 0 inspects 32 predecessors per
+// step and stops at the nearest one holding an inclusive prefix.  Load and store are
+// functors, so a scan can be fused with its producer (load) and consumer (store) -- e.g.
+// the preorder pass of the rooting stage.  A store must only touch its own tile's items:
+// the look-back orders status words, not other tiles' data.
 #pragma once
 #include <cub/block/block_scan.cuh>
 #include "common.cuh"
@@ -60,26 +63,37 @@ k_scan(i64 nitems, u64* status, T identity, Op op, LoadF load, StoreF store, T* 
     }
     T excl, total;
     BS(tmp).ExclusiveScan(acc, excl, identity, op, total);
-    if (tid == 0) {
-        T prefix = identity;
+    if (tid < 32) {
+        // warp 0 publishes, then looks back over 32 predecessors at a time
         u64* st = status + 1;
+        T prefix = identity;
         if (tile == 0) {
-            st_volatile_u64(st, (2ull << 62) | ((u64)total & SCAN_VMASK));
+            if (tid == 0) st_volatile_u64(st, (2ull << 62) | ((u64)total & SCAN_VMASK));
         } else {
-            st_volatile_u64(st + tile, (1ull << 62) | ((u64)total & SCAN_VMASK));
-            i64 j = tile - 1;
+            if (tid == 0) st_volatile_u64(st + tile, (1ull << 62) | ((u64)total & SCAN_VMASK));
+            i64 j = tile - 1;   // lane l looks at tile j - l
             for (;;) {
-                u64 s = ld_volatile_u64(st + j);
-                u64 f = s >> 62;
-                if (f == 0) continue;
-                prefix = op((T)(s & SCAN_VMASK), prefix);
-                if (f == 2) break;
-                --j;
+                i64 t = j - tid;
+                u64 sv;
+                do {
+                    sv = t >= 0 ? ld_volatile_u64(st + t) : (2ull << 62);
+                } while (__any_sync(0xFFFFFFFFu, (sv >> 62) == 0));
+                unsigned inc = __ballot_sync(0xFFFFFFFFu, (sv >> 62) == 2);
+                // lanes up to and including the nearest inclusive predecessor contribute
+                int last = inc ? __ffs(inc) - 1 : 31;
+                T pv = tid <= last ? (T)(sv & SCAN_VMASK) : identity;
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) pv = op(pv, (T)__shfl_xor_sync(0xFFFFFFFFu, pv, o));
+                prefix = op(prefix, pv);
+                if (inc) break;
+                j -= 32;
             }
-            st_volatile_u64(st + tile, (2ull << 62) | ((u64)op(prefix, total) & SCAN_VMASK));
+            if (tid == 0) st_volatile_u64(st + tile, (2ull << 62) | ((u64)op(prefix, total) & SCAN_VMASK));
         }
-        s_prefix = prefix;
-        if (total_out && tile == ntiles - 1) *total_out = op(prefix, total);
+        if (tid == 0) {
+            s_prefix = prefix;
+            if (total_out && tile == ntiles - 1) *total_out = op(prefix, total);
+        }
     }
     __syncthreads();
     T run = op(s_prefix, excl);
