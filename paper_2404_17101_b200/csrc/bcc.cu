@@ -32,8 +32,17 @@
 namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
-constexpr int NSAMPLE = 2;             // neighbours linked per vertex before giant detection
-constexpr u32 LR_K = 64;               // list-ranking ruler spacing (power of two)
+#ifndef PG_NSAMPLE
+#define PG_NSAMPLE 2
+#endif
+#ifndef PG_LR_K
+#define PG_LR_K 64
+#endif
+#ifndef PG_LOCAL_LB
+#define PG_LOCAL_LB 12
+#endif
+constexpr int NSAMPLE = PG_NSAMPLE;    // neighbours linked per vertex before giant detection
+constexpr u32 LR_K = PG_LR_K;          // list-ranking ruler spacing (power of two)
 constexpr int GIANT_SAMPLES = 1024;
 constexpr int HEAVY_GRID = 148 * 4;
 
@@ -158,7 +167,7 @@ __global__ void k_canon_init(i64 n, u32* UCNT, u32* CANON) {
 // edges in shared memory, then publishes flat parents P[v] = block root.  Chains along the
 // block (grid rows, preorder paths) collapse at shared-memory latency instead of walking
 // global memory; only block-crossing edges reach the global union-find.
-constexpr int LOCAL_LB = 12;
+constexpr int LOCAL_LB = PG_LOCAL_LB;
 constexpr int LOCAL_B = 1 << LOCAL_LB;
 constexpr int LOCAL_T = 512;
 

@@ -17,7 +17,10 @@
 namespace pg {
 
 constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_IPT = 8;
+#ifndef PG_SCAN_IPT
+#define PG_SCAN_IPT 8
+#endif
+constexpr int SCAN_IPT = PG_SCAN_IPT;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_IPT;
 constexpr u64 SCAN_VMASK = (1ull << 62) - 1;
 
