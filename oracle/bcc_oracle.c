@@ -52,39 +52,49 @@ static int twin_and_symmetry(int64_t n, const int64_t* off, const uint32_t* tgt,
     int64_t m = off[n];
     *status = ORC_OK;
     if (m == 0) return 1;
-    int64_t* fwd = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
-    int64_t* rev = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
-    int64_t* cnt = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
-    if (!fwd || !rev || !cnt) { free(fwd); free(rev); free(cnt); *status = ORC_NOMEM; return 0; }
-    for (int64_t e = 0; e < m; ++e) fwd[e] = e;
-    for (int64_t u = 0; u < n; ++u) {
-        if (!row_sorted(tgt, off[u], off[u + 1])) {
-            g_sort_tgt = tgt;
-            qsort(fwd + off[u], (size_t)(off[u + 1] - off[u]), sizeof(int64_t), cmp_slot_by_dst);
+    /* fwd = np.lexsort((dst, src)): slots ordered by (src, dst), stable.  Rows of a CSR
+     * are already grouped by src, so fwd is the identity unless some row is unsorted;
+     * only then is it materialised (int64, per-row stable sort by dst). */
+    int sorted_rows = 1;
+    for (int64_t u = 0; u < n && sorted_rows; ++u) sorted_rows = row_sorted(tgt, off[u], off[u + 1]);
+    int64_t* fwd = NULL;
+    if (!sorted_rows) {
+        fwd = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
+        if (!fwd) { *status = ORC_NOMEM; return 0; }
+        for (int64_t e = 0; e < m; ++e) fwd[e] = e;
+        for (int64_t u = 0; u < n; ++u) {
+            if (!row_sorted(tgt, off[u], off[u + 1])) {
+                g_sort_tgt = tgt;
+                qsort(fwd + off[u], (size_t)(off[u + 1] - off[u]), sizeof(int64_t), cmp_slot_by_dst);
+            }
         }
     }
     /* rev = np.lexsort((src, dst)): order by (dst, src, slot).  A stable counting sort
      * by dst over slots in increasing slot order gives it, because src is
-     * non-decreasing in slot order. */
+     * non-decreasing in slot order.  Slot ids fit uint32 (m < 2^32). */
+    uint32_t* rev = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m);
+    int64_t* cnt = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+    if (!rev || !cnt) { free(fwd); free(rev); free(cnt); *status = ORC_NOMEM; return 0; }
     for (int64_t e = 0; e < m; ++e) {
         if (tgt[e] >= (uint64_t)n) { free(fwd); free(rev); free(cnt); return 0; }
         cnt[tgt[e] + 1]++;
     }
     for (int64_t v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
-    for (int64_t e = 0; e < m; ++e) rev[cnt[tgt[e]]++] = e;
-    /* symmetric iff sorted (src,dst) keys == sorted (dst,src) keys, position by position */
+    for (int64_t e = 0; e < m; ++e) rev[cnt[tgt[e]]++] = (uint32_t)e;
+    /* symmetric iff sorted (src,dst) keys == sorted (dst,src) keys, position by position;
+     * twin[fwd[k]] = rev[k] (the reference's pairing). */
     int sym = 1;
-    int64_t u = 0;
-    /* src of fwd[k] is the row containing slot fwd[k]; fwd is row-grouped so walk rows */
+    int64_t u = 0, ru = 0;
     for (int64_t k = 0; k < m && sym; ++k) {
         while (off[u + 1] <= k) ++u;          /* fwd[k] lies in row u (fwd permutes within rows) */
-        int64_t ef = fwd[k], er = rev[k];
-        uint64_t fs = (uint64_t)u, fd = tgt[ef];
-        /* src of er: binary search the row containing slot er */
-        int64_t lo = 0, hi = n - 1;
-        while (lo < hi) { int64_t mid = (lo + hi + 1) / 2; if (off[mid] <= er) lo = mid; else hi = mid - 1; }
-        uint64_t rs = (uint64_t)lo, rd = tgt[er];
-        if (fs != rd || fd != rs) sym = 0;
+        int64_t ef = fwd ? fwd[k] : k, er = rev[k];
+        /* src of er: rev is ordered by dst, so walk its row pointer forward when possible */
+        if (off[ru] > er || off[ru + 1] <= er) {
+            int64_t lo = 0, hi = n - 1;
+            while (lo < hi) { int64_t mid = (lo + hi + 1) / 2; if (off[mid] <= er) lo = mid; else hi = mid - 1; }
+            ru = lo;
+        }
+        if ((uint64_t)u != tgt[er] || (uint64_t)tgt[ef] != (uint64_t)ru) sym = 0;
         twin[ef] = (uint32_t)er;
     }
     free(fwd); free(rev); free(cnt);
@@ -118,8 +128,8 @@ int oracle_bcc_hopcroft_tarjan(int64_t n, const int64_t* off, const uint32_t* tg
         free(twin);
         return st ? st : ORC_NOT_SYMMETRIC;
     }
-    int64_t* disc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
-    int64_t* low = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    int32_t* disc = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));   /* n < 2^31 */
+    int32_t* low = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
     int64_t* frame_v = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
     int64_t* frame_e = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
     int64_t* frame_pe = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
@@ -130,7 +140,8 @@ int oracle_bcc_hopcroft_tarjan(int64_t n, const int64_t* off, const uint32_t* tg
     }
     for (int64_t v = 0; v < n; ++v) { disc[v] = -1; low[v] = 0; articulation[v] = 0; }
     for (int64_t e = 0; e < m; ++e) edge_label[e] = -1;
-    int64_t timer = 0, comp_count = 0;
+    int32_t timer = 0;
+    int64_t comp_count = 0;
     int64_t fs = 0;       /* frame stack size */
     int64_t es = 0;       /* edge stack size */
 

@@ -39,7 +39,7 @@ constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual 
 #define PG_LR_K 64
 #endif
 #ifndef PG_LOCAL_LB
-#define PG_LOCAL_LB 12
+#define PG_LOCAL_LB 13
 #endif
 constexpr int NSAMPLE = PG_NSAMPLE;    // neighbours linked per vertex before giant detection
 constexpr u32 LR_K = PG_LR_K;          // list-ranking ruler spacing (power of two)
