@@ -379,16 +379,31 @@ def run_batch(args, rank, world, local):
     torch.cuda.synchronize()
     nmax = max((g.n for g in graphs), default=1)
     mmax = max((g.m for g in graphs), default=1)
-    ws = torch.empty(pg.workspace_bytes(nmax, mmax), dtype=torch.uint8, device=dev)
-    out = pg.DeviceBcc(edge_label=torch.empty(mmax, dtype=torch.int32, device=dev),
-                       artic_bits=torch.empty((nmax + 31) // 32, dtype=torch.int32, device=dev),
-                       bcc_count=torch.empty(1, dtype=torch.int64, device=dev))
+    # independent instances run concurrently on S streams (each with its own workspace and
+    # outputs): a single 4096^2 grid is latency-bound and leaves the GPU partly idle
+    S = max(1, min(args.streams, len(graphs)))
+    streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
+    wss = [torch.empty(pg.workspace_bytes(nmax, mmax), dtype=torch.uint8, device=dev) for _ in range(S)]
+    outs = [pg.DeviceBcc(edge_label=torch.empty(mmax, dtype=torch.int32, device=dev),
+                         artic_bits=torch.empty((nmax + 31) // 32, dtype=torch.int32, device=dev),
+                         bcc_count=torch.empty(1, dtype=torch.int64, device=dev)) for _ in range(S)]
     launches = 0
+    main_stream = torch.cuda.current_stream(dev)
 
     def step():
         nl = 0
-        for g in graphs:
-            nl += pg.bcc_device(g.offsets, g.targets, out=out, workspace=ws).launches
+        ev = torch.cuda.Event()
+        ev.record(main_stream)
+        for st in streams:
+            st.wait_event(ev)
+        for i, g in enumerate(graphs):
+            k = i % S
+            with torch.cuda.stream(streams[k]):
+                nl += pg.bcc_device(g.offsets, g.targets, out=outs[k], workspace=wss[k]).launches
+        for st in streams:
+            e = torch.cuda.Event()
+            e.record(st)
+            main_stream.wait_event(e)
         return nl
 
     for _ in range(args.warmup):
@@ -417,6 +432,7 @@ def run_batch(args, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": f"c5b: batch of {args.instances} grid 4096x4096 p=0.6 instances, seeds 1..{args.instances}",
+                       "streams_per_gpu": S,
                        "instances_per_s": args.instances * args.steps / (total_ms / 1e3),
                        "l2": "inputs larger than L2 (batch of 64 x 295 MB CSR)"},
             "gpu_launches": launches, "clocks": clocks,
@@ -465,6 +481,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5a", choices=["c1", "c2", "c3", "c4", "c5a", "c5b"])
     ap.add_argument("--instances", type=int, default=64, help="c5b: batch size (grid instances)")
+    ap.add_argument("--streams", type=int, default=4, help="c5b: concurrent instances per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0, help="sampling seed of the BCC call")
     ap.add_argument("--e2e-steps", type=int, default=2)

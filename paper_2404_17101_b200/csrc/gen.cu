@@ -1,13 +1,16 @@
-// gen.cu -- device graph construction (north-star subsystem 1): seeded generators and
-// the CSR builder (symmetrise + dedup + sort), replacing the reference's host
-// from_edges / symmetrize (graph.py:176-194, 452-481) and gen_grid (graph.py:488-508).
+// gen.cu -- device graph construction (north-star subsystem 1): seeded generators and the
+// CSR builder (own LSD radix sort, sort.cu, + fused dedup/offset scans), replacing the
+// reference's host from_edges / symmetrize (graph.py:176-194, 452-481) and gen_grid
+// (graph.py:488-508).
 // Generator rules are pinned in DESIGN.md "Generators"; host twins: oracle/gen_host.c.
-#include <cub/device/device_radix_sort.cuh>
 #include "common.cuh"
 #include "scan.cuh"
 #include "../../include/pasgal_bcc.h"
 
 namespace pg {
+
+size_t radix_sort_temp_bytes(i64 nkeys);
+cudaError_t radix_sort_edge_keys(u64* keys, u64* alt, i64 nkeys, int vb, void* temp, u64** result, cudaStream_t st);
 
 constexpr u64 KEY_SENTINEL = ~0ull;   // dropped key (self-loop / missing neighbour)
 
@@ -323,34 +326,20 @@ struct RevStore {
     __device__ __forceinline__ void operator()(i64 i, u64 ex, u64 v) const { off[n - i] = (i64)(ex < v ? ex : v); }
 };
 
-static size_t sort_temp_bytes(i64 nkeys, int bits) {
-    size_t b = 0;
-    cub::DoubleBuffer<u64> db(nullptr, nullptr);
-    cub::DeviceRadixSort::SortKeys(nullptr, b, db, nkeys, 0, bits);
-    return b;
-}
-
 size_t csr_build_temp_bytes(i64 n, i64 nkeys) {
-    int bits = 32 + vbits(n);
-    size_t s = sort_temp_bytes(nkeys > 0 ? nkeys : 1, bits);
-    size_t sc = scan_status_bytes((nkeys > n + 1 ? nkeys : n + 1));
-    return ((s + 255) & ~(size_t)255) + sc + 512;
+    size_t srt = radix_sort_temp_bytes(nkeys > 0 ? nkeys : 1);
+    size_t sc = scan_status_bytes(nkeys > n + 1 ? nkeys : n + 1);
+    return ((srt + 255) & ~(size_t)255) + sc + 512;
 }
 
 int csr_from_keys(i64 n, u64* keys, u64* keys_alt, i64 nkeys, i64* off, int32_t* tgt, i64* m_dev, void* temp,
                   size_t temp_bytes, cudaStream_t st) {
     if (n < 0 || n >= ((i64)1 << 31) || nkeys < 0) return PASGAL_EINVAL;
     if (temp_bytes < csr_build_temp_bytes(n, nkeys)) return PASGAL_EWORKSPACE;
-    int bits = 32 + vbits(n);
-    size_t sb = sort_temp_bytes(nkeys > 0 ? nkeys : 1, bits);
-    char* sort_tmp = (char*)temp;
-    u64* status = (u64*)((char*)temp + ((sb + 255) & ~(size_t)255));
-    const u64* sorted = keys;
-    if (nkeys > 0) {
-        cub::DoubleBuffer<u64> db(keys, keys_alt);
-        PG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(sort_tmp, sb, db, nkeys, 0, bits, st));
-        sorted = db.Current();
-    }
+    size_t srt = radix_sort_temp_bytes(nkeys > 0 ? nkeys : 1);
+    u64* status = (u64*)((char*)temp + ((srt + 255) & ~(size_t)255));
+    u64* sorted = keys;
+    if (nkeys > 0) PG_CUDA_TRY(radix_sort_edge_keys(keys, keys_alt, nkeys, vbits(n), temp, &sorted, st));
     // offsets[0..n-1] = "none yet"; offsets[n] = M (set by the unique scan's total)
     k_fill_i64<<<(unsigned)cdiv(n + 1, 256), 256, 0, st>>>(off, n + 1, (i64)SCAN_VMASK);
     PG_CUDA_TRY(launch_scan<u64>(nkeys, status, 0ull, SumOp(), UniqLoad{sorted}, UniqStore{sorted, tgt, off},
