@@ -559,6 +559,20 @@ __device__ __forceinline__ void warp_seg_minmax(int r, u32& mn, u32& mx, int lan
     }
 }
 
+__device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u32 mn, u32 mx, bool atomic) {
+    u32 f = __ldg(FIRST + row);
+    if (atomic) {
+        atomicMin(&W[f].x, mn);
+        atomicMax(&W[f].y, mx);
+    } else {
+        W[f] = make_uint2(mn < f ? mn : f, mx > f ? mx : f);
+    }
+}
+
+// The row running past a window edge carries its min/max to the next window of the chunk
+// in registers (warp-uniform), so a long row costs one atomic pair per 256-slot chunk
+// instead of one per window.  A row is stored without atomics when it begins and ends in
+// this chunk; a row that may extend into a neighbouring chunk uses atomics.
 __global__ void __launch_bounds__(WCH_BLOCK) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                     i64 n, i64 m, const u32* __restrict__ crow,
                                                     const u32* __restrict__ FIRST, uint2* W) {
@@ -578,6 +592,8 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_tags(const i64* __restrict__ off,
         if (s < s1) fw[k] = __ldg(FIRST + fw[k]);
     }
     u32 cur = crow[c];
+    u32 crw = PG_INV, cmn = PG_INV, cmx = 0;   // carried row and its running min/max
+    bool cbefore = false;                      // carried row began before this chunk
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         const i64 sb = s0 + 32 * k;
@@ -587,18 +603,34 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_tags(const i64* __restrict__ off,
         const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
         cur = __shfl_sync(0xFFFFFFFFu, row, 31);
         const Seg g = wc_segment(row, lane, valid, vm);
+        u32 mn = PG_INV, mx = 0;
         if (valid) {
-            u32 mn = __reduce_min_sync(g.mask, fw[k]);
-            u32 mx = __reduce_max_sync(g.mask, fw[k]);
-            if (lane == g.lo) {
-                u32 f = __ldg(FIRST + row);
-                if (!g.cut_left && !g.cut_right) {
-                    W[f] = make_uint2(mn < f ? mn : f, mx > f ? mx : f);
-                } else {
-                    atomicMin(&W[f].x, mn);
-                    atomicMax(&W[f].y, mx);
-                }
-            }
+            mn = __reduce_min_sync(g.mask, fw[k]);
+            mx = __reduce_max_sync(g.mask, fw[k]);
+        }
+        const u32 row0 = __shfl_sync(0xFFFFFFFFu, row, 0);
+        if (crw != PG_INV && crw != row0) {     // carried row ended at the previous window edge
+            if (lane == 0) write_tag(W, FIRST, crw, cmn, cmx, cbefore);
+            crw = PG_INV;
+        }
+        const bool merged = crw != PG_INV;       // then crw == row0: the first segment continues it
+        if (merged && g.lo == 0) {
+            mn = mn < cmn ? mn : cmn;
+            mx = mx > cmx ? mx : cmx;
+        }
+        // began before this chunk: only the first segment of the first window can (unknown,
+        // so assumed), or a merged carry that did
+        const bool before = g.lo == 0 && (merged ? cbefore : k == 0);
+        const bool has_next = sb + 32 < s1;      // window full and more of the chunk follows
+        if (valid && lane == g.lo && !(g.cut_right && has_next))
+            write_tag(W, FIRST, row, mn, mx, before || g.cut_right);
+        if (has_next) {                          // lane 31's segment continues: carry it
+            crw = __shfl_sync(0xFFFFFFFFu, row, 31);
+            cmn = __shfl_sync(0xFFFFFFFFu, mn, 31);
+            cmx = __shfl_sync(0xFFFFFFFFu, mx, 31);
+            cbefore = __shfl_sync(0xFFFFFFFFu, (int)before, 31) != 0;
+        } else {
+            crw = PG_INV;
         }
     }
 }

@@ -44,9 +44,12 @@ __global__ void k_chunk_rows(const i64* __restrict__ off, i64 n, i64 m, i64 nch,
 }
 
 // Row of slot s_base+lane for every valid lane (valid lanes are a prefix of the warp).
-// `cur` <= row of s_base on entry.  Must be called by all 32 lanes.
+// `cur` <= row of s_base on entry.  Must be called by all 32 lanes.  Fast path: when the
+// current row covers the whole window (long rows: most slots of a power-law graph) one
+// broadcast load decides it and no search runs.
 __device__ __forceinline__ u32 wc_resolve_row(const i64* __restrict__ off, i64 n, u32 cur, i64 s_base, int lane,
                                               bool valid) {
+    if (off[(i64)cur + 1] >= s_base + 32) return cur;   // warp-uniform
     u32 row = 0;
     bool done = !valid;
     u32 c = cur;

@@ -103,3 +103,86 @@ def test_mostly_empty_rows():
         off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
         if off[-1]:
             check_csr(off)
+
+
+def emulate_tags(off, vals, first):
+    """Lane-exact emulation of k_tags' segment reduce + carry/flush/atomic write protocol.
+    Returns W (min, max) per row; W starts at (first, first) like the preorder pass."""
+    n = off.shape[0] - 1
+    m = int(off[-1])
+    W = [[int(first[r]), int(first[r])] for r in range(n)]
+    stores = {}                     # rows written without atomics (must be written once)
+
+    def write(row, mn, mx, atomic):
+        f = int(first[row])
+        if atomic:
+            W[row][0] = min(W[row][0], mn)
+            W[row][1] = max(W[row][1], mx)
+        else:
+            assert row not in stores, "non-atomic store twice"
+            stores[row] = True
+            W[row] = [min(mn, f), max(mx, f)]
+
+    for c in range((m + WCH - 1) // WCH):
+        s0, s1 = c * WCH, min(c * WCH + WCH, m)
+        cur = chunk_row(off, n, s0)
+        crw, cmn, cmx, cbefore = None, None, None, False
+        for k in range(8):
+            sb = s0 + 32 * k
+            if sb >= s1:
+                break
+            valid = [sb + lane < s1 for lane in range(32)]
+            rows = resolve(off, n, cur, sb, valid)
+            cur = rows[31]
+            segs = segments(rows, valid)
+            mn = [None] * 32
+            mx = [None] * 32
+            for lane in range(32):
+                if valid[lane]:
+                    lo, hi, _, _ = segs[lane]
+                    seg_vals = [vals[sb + i] for i in range(lo, hi + 1)]
+                    mn[lane], mx[lane] = min(seg_vals), max(seg_vals)
+            row0 = rows[0]
+            if crw is not None and crw != row0:
+                write(crw, cmn, cmx, cbefore)
+                crw = None
+            merged = crw is not None
+            before = [False] * 32
+            for lane in range(32):
+                lo = segs[lane][0]
+                if merged and lo == 0 and valid[lane]:
+                    mn[lane], mx[lane] = min(mn[lane], cmn), max(mx[lane], cmx)
+                before[lane] = lo == 0 and (cbefore if merged else k == 0)
+            has_next = sb + 32 < s1
+            for lane in range(32):
+                lo, hi, _, cut_right = segs[lane]
+                if valid[lane] and lane == lo and not (cut_right and has_next):
+                    write(rows[lane], mn[lane], mx[lane], before[lane] or cut_right)
+            if has_next:
+                crw, cmn, cmx, cbefore = rows[31], mn[31], mx[31], before[31]
+            else:
+                crw = None
+    return W
+
+
+def test_tags_write_protocol():
+    rng = np.random.default_rng(3)
+    for trial in range(25):
+        n = int(rng.integers(20, 400))
+        deg = np.where(rng.random(n) < 0.5, 0, rng.integers(1, 12, n))
+        if trial % 3 == 0:
+            deg[int(rng.integers(0, n))] = int(rng.integers(200, 900))   # hub spanning chunks
+        if trial % 4 == 0:
+            deg[rng.integers(0, n, 5)] = 32                              # exact window sizes
+        off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        m = int(off[-1])
+        if m == 0:
+            continue
+        vals = rng.integers(0, 10 * n, m)
+        first = rng.permutation(n)
+        W = emulate_tags(off, vals, first)
+        for r in range(n):
+            seg = vals[off[r]:off[r + 1]]
+            want = [int(first[r]), int(first[r])] if seg.shape[0] == 0 else \
+                [min(int(first[r]), int(seg.min())), max(int(first[r]), int(seg.max()))]
+            assert W[r] == want, (trial, r)
