@@ -839,16 +839,13 @@ __global__ void k_cc2_rest_heavy(const i64* __restrict__ off, const int32_t* __r
     }
 }
 
-// final roots; CIDV[v] = preorder rank of the head of v's skeleton component
-__global__ void k_compress_final(i64 n, u32* C, const u32* __restrict__ PV, u32* CIDV, Ctr* ctr, u32* out_comp) {
+// final roots over positions (coalesced) + component count
+__global__ void k_compress_final(i64 n, u32* C, Ctr* ctr) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     u32 isroot = 0;
     if (i < n) {
         u32 c = uf_find(C, (u32)i);
         stcg(C + i, c);
-        u32 v = PV[i];
-        CIDV[v] = c;
-        if (out_comp) out_comp[v] = c;
         isroot = c == (u32)i;
     }
     u32 cnt = __popc(__ballot_sync(0xFFFFFFFFu, isroot));
@@ -879,13 +876,20 @@ __global__ void k_artic(i64 n, const u32* __restrict__ PPAR, const u32* __restri
     }
 }
 
-// the giant skeleton component's final id and its membership bitmap (one ballot per word)
-__global__ void k_giant_bits(i64 n, const u32* __restrict__ C, const u32* __restrict__ CIDV, Ctr* ctr, u32* GBIT) {
+// per vertex (coalesced): CIDV[v] = component of position first[v] (one random read of the
+// compressed C), plus the giant component's membership bitmap (one ballot per word)
+__global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __restrict__ FIRST, Ctr* ctr, u32* CIDV,
+                               u32* GBIT, u32* out_comp) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const u32 g = C[ctr->giant2];        // C is fully compressed: the root of the sampled giant
     if (v == 0) ctr->gcid = g;
-    bool in = v < n && CIDV[v] == g;
-    unsigned b = __ballot_sync(0xFFFFFFFFu, in);
+    u32 cid = PG_INV;
+    if (v < n) {
+        cid = __ldg(C + __ldg(FIRST + v));
+        CIDV[v] = cid;
+        if (out_comp) out_comp[v] = cid;
+    }
+    unsigned b = __ballot_sync(0xFFFFFFFFu, cid == g);
     if ((threadIdx.x & 31) == 0 && v < n) GBIT[v >> 5] = b;
 }
 
@@ -1176,8 +1180,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
-    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.PV, w.CIDV, w.ctr, out->comp));
-    PG_K(k_giant_bits<<<nblk(n, B), B, 0, st>>>(n, w.C, w.CIDV, w.ctr, w.GBIT));
+    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.ctr));
+    PG_K(k_cid_vertices<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FIRST, w.ctr, w.CIDV, w.GBIT, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
     // ---- S6 articulation, labels, count
