@@ -461,6 +461,16 @@ def run_e2e(args, dg, dev, n, m):
     steps = max(1, min(args.steps, args.e2e_steps))
     res = pg.bcc(g, device=dev, host_out=hb)         # warm-up
     torch.cuda.synchronize()
+    # split-out components (diagnostic only): H2D copy and device validation alone
+    t0 = time.perf_counter()
+    off_d = off_h.to(dev, non_blocking=True)
+    tgt_d = tgt_h.to(dev, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pg.validate_device(off_d, tgt_d)
+    val_s = time.perf_counter() - t0
+    del off_d, tgt_d
     t0 = time.perf_counter()
     for _ in range(steps):
         res = pg.bcc(g, device=dev, host_out=hb)
@@ -470,6 +480,7 @@ def run_e2e(args, dg, dev, n, m):
     del res
     return {"value": (m // 2) / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps,
+            "h2d_ms": round(h2d_s * 1e3, 1), "validate_ms": round(val_s * 1e3, 1),
             "path": "paper_2404_17101_b200.bcc(g) with host numpy CSR (pinned) -> H2D, validate, FAST-BCC, "
                     "D2H labels+bitmap+count (pinned)"}
 
