@@ -1044,14 +1044,20 @@ __device__ __forceinline__ i64 lower_bound_row(const int32_t* tgt, i64 a, i64 b,
     return a;
 }
 
+// Exact multiset symmetry with half the searches: every slot u->w with u < w must find its
+// own copy of u in row w (the k-th copy of w in row u pairs with the k-th copy of u in row
+// w: an injection from "up" slots to "down" slots), and the numbers of up and down slots
+// must be equal, which makes the injection a bijection.  The search runs in row w, the
+// larger id -- rarely a hub row in power-law graphs, whose hubs have small ids.
 __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                              i64 n, i64 m, const u32* __restrict__ crow, Ctr* ctr) {
+                                                              i64 n, i64 m, const u32* __restrict__ crow, Ctr* ctr,
+                                                              unsigned long long* updown) {
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     u32 cur = crow[c];
-    u32 err = 0;
+    u32 err = 0, nup = 0, ndown = 0;
 #pragma unroll 1
     for (i64 sb = s0; sb < s1; sb += 32) {
         const i64 s = sb + lane;
@@ -1062,16 +1068,25 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restr
         const i64 u = row;
         int32_t w = tgt[s];
         if (w < 0 || (i64)w >= n) { err |= VERR_RANGE; continue; }
-        i64 rs = off[u], re = off[u + 1];
+        i64 re = off[u + 1];
         if (s + 1 < re && tgt[s + 1] < w) { err |= VERR_UNSORTED; continue; }
-        // multiset symmetry: the k-th copy of w in row u needs a k-th copy of u in row w
-        i64 k = s - lower_bound_row(tgt, rs, s, w);
+        if ((i64)w < u) { ++ndown; continue; }
+        if ((i64)w == u) continue;   // self-loop: its own reverse
+        ++nup;
+        i64 rs = off[u], k = 0;
+        while (s - k - 1 >= rs && tgt[s - k - 1] == w) ++k;   // copy index of w in row u
         i64 ws = off[w], we = off[w + 1];
         i64 q = lower_bound_row(tgt, ws, we, (int32_t)u) + k;
         if (q >= we || tgt[q] != (int32_t)u) err |= VERR_NOTSYM;
     }
     err = __reduce_or_sync(0xFFFFFFFFu, err);
-    if (lane == 0 && err) atomicOr(&ctr->verr, err);
+    nup = __reduce_add_sync(0xFFFFFFFFu, nup);
+    ndown = __reduce_add_sync(0xFFFFFFFFu, ndown);
+    if (lane == 0) {
+        if (err) atomicOr(&ctr->verr, err);
+        if (nup) atomicAdd(updown, (unsigned long long)nup);
+        if (ndown) atomicAdd(updown + 1, (unsigned long long)ndown);
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -1230,11 +1245,16 @@ int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStrea
     PG_CUDA_TRY(cudaStreamSynchronize(st));
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (m > 0 && n > 0) {
+        unsigned long long* updown = (unsigned long long*)w.SCAN;   // scratch: 2 counters
+        PG_CUDA_TRY(cudaMemsetAsync(updown, 0, 2 * sizeof(unsigned long long), st));
         k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(g->offsets, n, m, w.nch, w.CROW);
-        k_validate_slots<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.CROW, w.ctr);
+        k_validate_slots<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.CROW, w.ctr, updown);
         PG_LAUNCH_CHECK();
+        unsigned long long ud[2];
         PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+        PG_CUDA_TRY(cudaMemcpyAsync(ud, updown, sizeof ud, cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaStreamSynchronize(st));
+        if (!(h.verr & (VERR_RANGE | VERR_UNSORTED)) && ud[0] != ud[1]) h.verr |= VERR_NOTSYM;
     }
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
