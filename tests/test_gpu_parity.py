@@ -112,6 +112,16 @@ def test_validation_errors_match_reference():
     tgt = np.array([1], dtype=np.uint32)
     with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
         pg.bcc(pg.Graph(off, tgt))
+    # up/down slot counts balance but the partners do not match
+    off = np.array([0, 1, 1, 2], dtype=np.int64)
+    tgt = np.array([1, 0], dtype=np.uint32)
+    with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
+        pg.bcc(pg.Graph(off, tgt))
+    # a parallel edge present twice one way, once the other way
+    off = np.array([0, 2, 3], dtype=np.int64)
+    tgt = np.array([1, 1, 0], dtype=np.uint32)
+    with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
+        pg.bcc(pg.Graph(off, tgt))
     # unsorted row
     off = np.array([0, 2, 3, 4], dtype=np.int64)
     tgt = np.array([2, 1, 0, 0], dtype=np.uint32)
