@@ -1064,8 +1064,10 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restr
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         lo[k] = hi[k] = 0;
-        uu[k] = 0;
-        kk[k] = 0;
+        uu[k] = kk[k] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) {
         const i64 sb = s0 + 32 * k;
         if (sb >= s1) break;   // warp-uniform
         const i64 s = sb + lane;
