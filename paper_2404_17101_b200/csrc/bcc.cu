@@ -1058,18 +1058,8 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restr
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     u32 cur = crow[c];
     u32 err = 0, nup = 0, ndown = 0;
-    // phase 1: per window, local checks and the search range of every up slot
-    i64 lo[WCH_U], hi[WCH_U];
-    u32 uu[WCH_U], kk[WCH_U];
-#pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        lo[k] = hi[k] = 0;
-        uu[k] = kk[k] = 0;
-    }
-#pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        const i64 sb = s0 + 32 * k;
-        if (sb >= s1) break;   // warp-uniform
+#pragma unroll 1
+    for (i64 sb = s0; sb < s1; sb += 32) {
         const i64 s = sb + lane;
         const bool valid = s < s1;
         const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
@@ -1078,43 +1068,16 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restr
         const i64 u = row;
         int32_t w = tgt[s];
         if (w < 0 || (i64)w >= n) { err |= VERR_RANGE; continue; }
-        if (s + 1 < off[u + 1] && tgt[s + 1] < w) { err |= VERR_UNSORTED; continue; }
+        i64 re = off[u + 1];
+        if (s + 1 < re && tgt[s + 1] < w) { err |= VERR_UNSORTED; continue; }
         if ((i64)w < u) { ++ndown; continue; }
         if ((i64)w == u) continue;   // self-loop: its own reverse
         ++nup;
-        i64 rs = off[u];
-        u32 dup = 0;
-        while (s - dup - 1 >= rs && tgt[s - dup - 1] == w) ++dup;   // copy index of w in row u
-        lo[k] = off[w];
-        hi[k] = off[w + 1];
-        uu[k] = (u32)u;
-        kk[k] = dup + 1;   // 0 marks "no search"
-    }
-    // phase 2: the windows' lower_bound searches advance in lockstep (WCH_U probes in flight)
-    for (;;) {
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < WCH_U; ++k) any |= kk[k] && lo[k] < hi[k];
-        if (!__any_sync(0xFFFFFFFFu, any)) break;
-        int32_t probe[WCH_U];
-#pragma unroll
-        for (int k = 0; k < WCH_U; ++k) probe[k] = kk[k] && lo[k] < hi[k] ? tgt[(lo[k] + hi[k]) >> 1] : 0;
-#pragma unroll
-        for (int k = 0; k < WCH_U; ++k) {
-            if (kk[k] && lo[k] < hi[k]) {
-                i64 mid = (lo[k] + hi[k]) >> 1;
-                if (probe[k] < (int32_t)uu[k]) lo[k] = mid + 1; else hi[k] = mid;
-            }
-        }
-    }
-    // phase 3: the k-th copy of u must sit at lower_bound + k in row w
-#pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        if (!kk[k]) continue;
-        const i64 sb = s0 + 32 * k, s = sb + lane;
-        const u32 w = (u32)tgt[s];
-        i64 q = lo[k] + (kk[k] - 1);
-        if (q >= off[(i64)w + 1] || tgt[q] != (int32_t)uu[k]) err |= VERR_NOTSYM;
+        i64 rs = off[u], k = 0;
+        while (s - k - 1 >= rs && tgt[s - k - 1] == w) ++k;   // copy index of w in row u
+        i64 ws = off[w], we = off[w + 1];
+        i64 q = lower_bound_row(tgt, ws, we, (int32_t)u) + k;
+        if (q >= we || tgt[q] != (int32_t)u) err |= VERR_NOTSYM;
     }
     err = __reduce_or_sync(0xFFFFFFFFu, err);
     nup = __reduce_add_sync(0xFFFFFFFFu, nup);
