@@ -225,11 +225,44 @@ __global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* _
     }
 }
 
+// Full compression.  A find is a chain of dependent loads, so each thread walks
+// COMPRESS_ILP chains in lockstep (positions v, v+stride, ...) to keep several in flight.
+constexpr int COMPRESS_ILP = 4;
+
+__device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[COMPRESS_ILP], i64 (&idx)[COMPRESS_ILP]) {
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    u32 x[COMPRESS_ILP];
+#pragma unroll
+    for (int j = 0; j < COMPRESS_ILP; ++j) {
+        idx[j] = t + j * stride;
+        x[j] = idx[j] < n ? ldcg(P + idx[j]) : 0u;
+    }
+    bool more = true;
+    while (more) {
+        more = false;
+        u32 px[COMPRESS_ILP];
+#pragma unroll
+        for (int j = 0; j < COMPRESS_ILP; ++j) px[j] = idx[j] < n ? ldcg(P + x[j]) : x[j];
+#pragma unroll
+        for (int j = 0; j < COMPRESS_ILP; ++j) {
+            if (px[j] != x[j]) {
+                x[j] = px[j];
+                more = true;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < COMPRESS_ILP; ++j) {
+        root[j] = x[j];
+        if (idx[j] < n) stcg(P + idx[j], x[j]);
+    }
+}
+
 __global__ void k_compress(i64 n, u32* P) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    u32 r = uf_find(P, (u32)v);
-    stcg(P + v, r);
+    u32 root[COMPRESS_ILP];
+    i64 idx[COMPRESS_ILP];
+    compress_ilp(n, P, root, idx);
 }
 
 // most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root)
@@ -792,13 +825,16 @@ __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* 
     if (u >= n) return;
     i64 a = off[u], b = off[u + 1];
     if (b - a < 2) return;     // a degree-1 vertex has only its tree edge
-    if (b > a + SCAN2) b = a + SCAN2;
+    const int cnt = (int)(b - a < SCAN2 ? b - a : SCAN2);
     uint2 fu = FL[u];
+    uint2 fw[SCAN2];           // all loads issued before the first test
+#pragma unroll
+    for (int k = 0; k < SCAN2; ++k) fw[k] = k < cnt ? FL[(u32)tgt[a + k]] : fu;
     int linked = 0;
-    for (i64 s = a; s < b && linked < NSAMPLE2; ++s) {
-        uint2 fw = FL[(u32)tgt[s]];
-        if (is_cross(fu, fw)) {
-            uf_link(C, fu.x, fw.x);
+#pragma unroll
+    for (int k = 0; k < SCAN2; ++k) {
+        if (linked < NSAMPLE2 && k < cnt && is_cross(fu, fw[k])) {
+            uf_link(C, fu.x, fw[k].x);
             ++linked;
         }
     }
@@ -839,16 +875,14 @@ __global__ void k_cc2_rest_heavy(const i64* __restrict__ off, const int32_t* __r
     }
 }
 
-// final roots over positions (coalesced) + component count
+// final roots over positions + component count
 __global__ void k_compress_final(i64 n, u32* C, Ctr* ctr) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    u32 isroot = 0;
-    if (i < n) {
-        u32 c = uf_find(C, (u32)i);
-        stcg(C + i, c);
-        isroot = c == (u32)i;
-    }
-    u32 cnt = __popc(__ballot_sync(0xFFFFFFFFu, isroot));
+    u32 root[COMPRESS_ILP];
+    i64 idx[COMPRESS_ILP];
+    compress_ilp(n, C, root, idx);
+    u32 cnt = 0;
+#pragma unroll
+    for (int j = 0; j < COMPRESS_ILP; ++j) cnt += __popc(__ballot_sync(0xFFFFFFFFu, idx[j] < n && root[j] == (u32)idx[j]));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr->ncomp, cnt);
 }
 
@@ -909,11 +943,22 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ of
     if (c >= num_chunks(m)) return;
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     const u32 g = ctr->gcid;
-    u32 w[WCH_U], cw[WCH_U];
+    u32 w[WCH_U], cw[WCH_U], rw[WCH_U];
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         i64 s = s0 + 32 * k + lane;
         w[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
+    }
+    // rows of all windows first: the offset loads and shuffles overlap the target loads
+    u32 cur = crow[c];
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) {
+        rw[k] = 0;
+        const i64 sb = s0 + 32 * k;
+        if (sb < s1) {   // warp-uniform
+            rw[k] = wc_resolve_row(off, n, cur, sb, lane, sb + lane < s1);
+            cur = __shfl_sync(0xFFFFFFFFu, rw[k], 31);
+        }
     }
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
@@ -925,19 +970,13 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ of
         i64 s = s0 + 32 * k + lane;
         cw[k] = (cw[k] >> (w[k] & 31)) & 1u ? g : (s < s1 ? __ldg(CIDV + w[k]) : 0u);
     }
-    u32 cur = crow[c];
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
-        const i64 sb = s0 + 32 * k;
-        if (sb >= s1) break;  // warp-uniform
-        const i64 s = sb + lane;
-        const bool valid = s < s1;
-        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
-        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
-        if (!valid) continue;
-        u32 cu = __ldg(CIDV + row);
+        const i64 s = s0 + 32 * k + lane;
+        if (s >= s1) break;
+        u32 cu = __ldg(CIDV + rw[k]);
         u32 lab = cu > cw[k] ? cu : cw[k];
-        if (w[k] == row) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
+        if (w[k] == rw[k]) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
         __stcs(label + s, lab);
     }
 }
@@ -1142,7 +1181,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
     PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
-    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.P));
+    PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
     PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
@@ -1191,11 +1230,11 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.C));
     PG_K(k_cc2_tree<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.C));
     PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
-    PG_K(k_compress<<<nblk(n, B), B, 0, st>>>(n, w.C));
+    PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
-    PG_K(k_compress_final<<<nblk(n, B), B, 0, st>>>(n, w.C, w.ctr));
+    PG_K(k_compress_final<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C, w.ctr));
     PG_K(k_cid_vertices<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FIRST, w.ctr, w.CIDV, w.GBIT, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
