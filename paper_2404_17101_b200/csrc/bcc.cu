@@ -349,28 +349,19 @@ __device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc
 }
 
 __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
-    // two vertices per thread (x and x + stride): four exchanges in flight
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    const i64 x0 = (i64)blockIdx.x * blockDim.x + threadIdx.x, x1 = x0 + stride;
+    i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    uint2 e0 = x0 < n ? HAB[x0] : make_uint2(PG_INV, PG_INV);
-    uint2 e1 = x1 < n ? HAB[x1] : make_uint2(PG_INV, PG_INV);
-    const bool a0 = e0.x != PG_INV, a1 = e1.x != PG_INV;
-    ArcGroup g0a = arc_group(e0.x, a0, lane), g0b = arc_group(e0.y, a0, lane);
-    ArcGroup g1a = arc_group(e1.x, a1, lane), g1b = arc_group(e1.y, a1, lane);
-    u32 o0a = 0, o0b = 0, o1a = 0, o1b = 0;
-    if (a0 && lane == g0a.lead) o0a = atomicExch(HEAD + e0.x, 2 * (u32)x0);       // a->b out of a
-    if (a0 && lane == g0b.lead) o0b = atomicExch(HEAD + e0.y, 2 * (u32)x0 + 1);   // b->a out of b
-    if (a1 && lane == g1a.lead) o1a = atomicExch(HEAD + e1.x, 2 * (u32)x1);
-    if (a1 && lane == g1b.lead) o1b = atomicExch(HEAD + e1.y, 2 * (u32)x1 + 1);
-    if (a0) {
-        arc_splice(NEXT, g0a, 2 * (u32)x0, o0a);
-        arc_splice(NEXT, g0b, 2 * (u32)x0 + 1, o0b);
-    }
-    if (a1) {
-        arc_splice(NEXT, g1a, 2 * (u32)x1, o1a);
-        arc_splice(NEXT, g1b, 2 * (u32)x1 + 1, o1b);
-    }
+    uint2 e = x < n ? HAB[x] : make_uint2(PG_INV, PG_INV);
+    const bool act = e.x != PG_INV;
+    const u32 arc_a = 2 * (u32)x, arc_b = 2 * (u32)x + 1;   // a->b out of a, b->a out of b
+    ArcGroup ga = arc_group(e.x, act, lane);
+    ArcGroup gb = arc_group(e.y, act, lane);
+    if (!act) return;
+    u32 olda = 0, oldb = 0;
+    if (lane == ga.lead) olda = atomicExch(HEAD + e.x, arc_a);
+    if (lane == gb.lead) oldb = atomicExch(HEAD + e.y, arc_b);
+    arc_splice(NEXT, ga, arc_a, olda);
+    arc_splice(NEXT, gb, arc_b, oldb);
 }
 
 // Close every out-arc list into a cycle (a root's cycle exits through its up arc) and set
@@ -468,46 +459,26 @@ __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, c
     return t.head != PG_INV && (t.head & (LR_K - 1)) != 0;
 }
 
-// Each thread walks LR_ILP rulers' sublists interleaved (more dependent loads in flight
-// than there are resident threads).
-constexpr int LR_ILP = 2;
-
 __global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
                            const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr, u32* SPLEN,
                            u32* SPNEXT) {
-    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    const TourInfo ti = tour_info(ctr, ROOTS, n);
-    u32 x[LR_ILP], cnt[LR_ILP];
-    bool live[LR_ILP];
-#pragma unroll
-    for (int j = 0; j < LR_ILP; ++j) {
-        const i64 s = t + j * stride;
-        cnt[j] = 0;
-        live[j] = s < ns && ruler_start(s, ns - 1, ti, HAB, HEAD, x[j]);
-        if (s < ns && !live[j]) {
-            SPLEN[s] = 0;
-            SPNEXT[s] = PG_INV;
-        }
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const TourInfo t = tour_info(ctr, ROOTS, n);
+    const i64 nsk = ns - 1;
+    u32 x;
+    if (!ruler_start(s, nsk, t, HAB, HEAD, x)) {
+        SPLEN[s] = 0;
+        SPNEXT[s] = PG_INV;
+        return;
     }
-    bool any = true;
-    while (any) {
-        any = false;
-#pragma unroll
-        for (int j = 0; j < LR_ILP; ++j) {
-            if (!live[j]) continue;
-            ++cnt[j];
-            x[j] = __ldg(NEXT + (x[j] ^ 1u));
-            if (x[j] == PG_INV || (x[j] & (LR_K - 1)) == 0) {   // the head is never revisited
-                const i64 s = t + j * stride;
-                SPLEN[s] = cnt[j];
-                SPNEXT[s] = x[j] == PG_INV ? PG_INV : x[j] / LR_K;
-                live[j] = false;
-            } else {
-                any = true;
-            }
-        }
-    }
+    u32 cnt = 0;
+    do {
+        ++cnt;
+        x = __ldg(NEXT + (x ^ 1u));
+    } while (x != PG_INV && (x & (LR_K - 1)) != 0);   // the head is never revisited
+    SPLEN[s] = cnt;
+    SPNEXT[s] = x == PG_INV ? PG_INV : x / LR_K;
 }
 
 // Wyllie pointer jumping on the rulers: suffix sums of sublist lengths
@@ -528,32 +499,19 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
 __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
                            const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr,
                            const u32* __restrict__ SUFFIX, u32* RANK, u32* TA) {
-    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    const TourInfo ti = tour_info(ctr, ROOTS, n);
-    u32 x[LR_ILP], pos[LR_ILP];
-    bool live[LR_ILP];
-#pragma unroll
-    for (int j = 0; j < LR_ILP; ++j) {
-        const i64 s = t + j * stride;
-        live[j] = s < ns && ruler_start(s, ns - 1, ti, HAB, HEAD, x[j]);
-        pos[j] = live[j] ? ti.len - SUFFIX[s] : 0u;
-    }
-    bool any = true;
-    while (any) {
-        any = false;
-#pragma unroll
-        for (int j = 0; j < LR_ILP; ++j) {
-            if (!live[j]) continue;
-            u32 nx = __ldg(NEXT + (x[j] ^ 1u));   // issue the chain load first
-            RANK[x[j]] = pos[j];
-            TA[pos[j]] = x[j];
-            ++pos[j];
-            x[j] = nx;
-            if (nx == PG_INV || (nx & (LR_K - 1)) == 0) live[j] = false;
-            else any = true;
-        }
-    }
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const TourInfo t = tour_info(ctr, ROOTS, n);
+    u32 x;
+    if (!ruler_start(s, ns - 1, t, HAB, HEAD, x)) return;
+    u32 pos = t.len - SUFFIX[s];
+    do {
+        u32 nx = __ldg(NEXT + (x ^ 1u));   // issue the chain load first
+        RANK[x] = pos;
+        TA[pos] = x;
+        ++pos;
+        x = nx;
+    } while (x != PG_INV && (x & (LR_K - 1)) != 0);
 }
 
 // preorder pass over tour positions, fused into a decoupled-look-back scan of the
@@ -1231,7 +1189,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
-    PG_K(k_arc_link<<<nblk(cdiv(n, 2), B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
     PG_CUDA_TRY(launch_scan<u64>(n, w.SCAN, 0ull, SumOp(), RootLoad{w.HAB, w.HEAD},
                                  RootStore{w.RIDX, w.ROOTS, w.ROOTMARK, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent,
                                            out->first},
@@ -1242,14 +1200,14 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
-    PG_K(k_lr_walk1<<<nblk(cdiv(w.ns, LR_ILP), 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[0],
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[0],
                                                      w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
         PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    PG_K(k_lr_walk2<<<nblk(cdiv(w.ns, LR_ILP), 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[cur],
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[cur],
                                                      w.RANK, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
