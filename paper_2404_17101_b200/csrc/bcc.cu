@@ -63,8 +63,8 @@ struct Ctr {
 // --------------------------------------------------------------------------
 struct Ws {
     u32 *P, *HEAD, *RIDX, *ROOTS;
-    uint2* HAB;
-    u32 *NEXT, *RANK;
+    uint2* HAB;   // per vertex v: HAB[2v] = hook edge {a, b}; HAB[2v+1] = tour positions of arcs 2v, 2v+1
+    u32* NEXT;
     u32 *SPLEN[2], *SPNEXT[2];
     u32* TA;      // arc at each tour position (walk2)
     u32* TP;      // parent (source vertex) of the arc at each tour position
@@ -106,12 +106,11 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
-    w.HAB = (uint2*)take(8 * nn);
+    w.HAB = (uint2*)take(16 * nn);
     w.HEAD = (u32*)take(4 * nn);
     w.RIDX = (u32*)take(4 * nn);
     w.ROOTS = (u32*)take(4 * nn);
     w.NEXT = (u32*)take(4 * L);
-    w.RANK = (u32*)take(4 * L);
     for (int b = 0; b < 2; ++b) {
         w.SPLEN[b] = (u32*)take(4 * w.ns);
         w.SPNEXT[b] = (u32*)take(4 * w.ns);
@@ -151,7 +150,7 @@ __global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C) {
     if (v >= n) return;
     P[v] = (u32)v;
     C[v] = (u32)v;
-    HAB[v] = make_uint2(PG_INV, PG_INV);
+    HAB[2 * v] = make_uint2(PG_INV, PG_INV);
     HEAD[v] = PG_INV;
 }
 
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restri
             i64 w = tgt[a + k];
             if ((w >> LOCAL_LB) != blockIdx.x) continue;
             u32 hi = slink(sp, (u32)i, (u32)(w - b0));
-            if (hi != PG_INV) HAB[b0 + hi] = make_uint2((u32)v, (u32)w);
+            if (hi != PG_INV) HAB[2 * (b0 + hi)] = make_uint2((u32)v, (u32)w);
         }
     }
     __syncthreads();
@@ -351,7 +350,7 @@ __device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc
 __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
     i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    uint2 e = x < n ? HAB[x] : make_uint2(PG_INV, PG_INV);
+    uint2 e = x < n ? HAB[2 * x] : make_uint2(PG_INV, PG_INV);
     const bool act = e.x != PG_INV;
     const u32 arc_a = 2 * (u32)x, arc_b = 2 * (u32)x + 1;   // a->b out of a, b->a out of b
     ArcGroup ga = arc_group(e.x, act, lane);
@@ -374,7 +373,7 @@ __global__ void k_arc_close(i64 n, const uint2* __restrict__ HAB, const u32* __r
                             const u32* __restrict__ ROOTS, const Ctr* ctr, u32* NEXT) {
     i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= n) return;
-    uint2 e = HAB[x];
+    uint2 e = HAB[2 * x];
     if (e.x != PG_INV) {
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
@@ -399,7 +398,7 @@ struct RootLoad {
     const uint2* HAB;
     const u32* HEAD;   // PG_INV: no forest arcs (isolated, or only self-loops)
     __device__ __forceinline__ u64 operator()(i64 v) const {
-        if (HAB[v].x != PG_INV) return 0;
+        if (HAB[2 * v].x != PG_INV) return 0;
         return HEAD[v] == PG_INV ? 1ull : (1ull << 31);
     }
 };
@@ -436,7 +435,7 @@ __global__ void k_roots_total(Ctr* ctr) {
 
 // ruling-set list ranking over succ(a) = NEXT[a^1].  Rulers: every on-tour arc a with
 // a % LR_K == 0, plus the head (ruler index nsk).  walk1: each ruler's sublist length and
-// next ruler; Wyllie on the rulers; walk2: final positions (RANK) and TA[position] = arc.
+// next ruler; Wyllie on the rulers; walk2: final positions (into HAB[2y+1]) and TA[position] = arc.
 struct TourInfo {
     u32 head;     // first arc of the list, PG_INV if the tour is empty
     u32 len;      // arcs on the tour = 2 * (n - isolated)
@@ -453,7 +452,7 @@ __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, c
     if (s < nsk) {
         x = (u32)s * LR_K;
         u32 v = x >> 1;
-        return !(HAB[v].x == PG_INV && HEAD[v] == PG_INV);   // isolated vertices are off the tour
+        return !(HAB[2 * (i64)v].x == PG_INV && HEAD[v] == PG_INV);   // isolated vertices are off the tour
     }
     x = t.head;
     return t.head != PG_INV && (t.head & (LR_K - 1)) != 0;
@@ -498,7 +497,7 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
 
 __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
                            const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr,
-                           const u32* __restrict__ SUFFIX, u32* RANK, u32* TA) {
+                           const u32* __restrict__ SUFFIX, uint2* HABW, u32* TA) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const TourInfo t = tour_info(ctr, ROOTS, n);
@@ -507,7 +506,7 @@ __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
     u32 pos = t.len - SUFFIX[s];
     do {
         u32 nx = __ldg(NEXT + (x ^ 1u));   // issue the chain load first
-        RANK[x] = pos;
+        reinterpret_cast<u32*>(HABW + 2 * (i64)(x >> 1) + 1)[x & 1u] = pos;   // position of arc x
         TA[pos] = x;
         ++pos;
         x = nx;
@@ -521,7 +520,6 @@ __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
 // items, which the look-back does not order.
 struct PreLoad {
     const u32* TA;
-    const u32* RANK;
     const uint2* HAB;
     u64* T;
     u32* TP;
@@ -532,8 +530,10 @@ struct PreLoad {
     __device__ __forceinline__ u32 operator()(i64 k) const {
         if (k >= 2 * (n - (i64)(ctr->roots & M31))) return 0u;
         u32 x = __ldg(TA + k);
-        u32 pt = __ldg(RANK + (x ^ 1u));
-        uint2 e = __ldg(HAB + (x >> 1));
+        // one 16-byte record: the hook edge and both arcs' positions
+        uint4 r = __ldg(reinterpret_cast<const uint4*>(HAB + 2 * (i64)(x >> 1)));
+        u32 pt = (x & 1u) ? r.z : r.w;   // the twin's position
+        uint2 e = make_uint2(r.x, r.y);
         u32 tg, src;
         if (e.x != PG_INV) {                 // tree arc 2y = a->b, 2y+1 = b->a
             tg = (x & 1u) ? e.x : e.y;
@@ -1208,10 +1208,10 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         cur ^= 1;
     }
     PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[cur],
-                                                     w.RANK, w.TA));
+                                                     w.HAB, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
-    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.RANK, w.HAB, w.T, w.TP, w.ctr, n},
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.HAB, w.T, w.TP, w.ctr, n},
                                  PreStore{w.T, w.TP, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
                                  (u32*)nullptr, st));
     ++nl;

@@ -70,14 +70,14 @@ __device__ __forceinline__ bool uf_link(u32* P, u32 a, u32 b) {
 }
 
 // link a-b and record the graph edge that caused the merge at the hooked root
-// (HAB[hi] = {a, b}; each vertex is hooked at most once, so HAB names a spanning forest)
+// (HAB[2 hi] = {a, b}; each vertex is hooked at most once, so HAB names a spanning forest)
 __device__ __forceinline__ void uf_link_hook(u32* P, u32 a, u32 b, uint2* HAB) {
     u32 ra = uf_find(P, a), rb = uf_find(P, b);
     while (ra != rb) {
         u32 hi = ra > rb ? ra : rb, lo = ra ^ rb ^ hi;
         u32 old = atomicCAS(P + hi, hi, lo);
         if (old == hi) {
-            HAB[hi] = make_uint2(a, b);
+            HAB[2 * (size_t)hi] = make_uint2(a, b);
             return;
         }
         ra = uf_find(P, ra);
