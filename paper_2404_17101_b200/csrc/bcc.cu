@@ -783,6 +783,9 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 #ifndef PG_SCAN2
 #define PG_SCAN2 4
 #endif
+#ifndef PG_SAMPLE2_MODE
+#define PG_SAMPLE2_MODE 0
+#endif
 constexpr int NSAMPLE2 = PG_NSAMPLE2;
 constexpr int SCAN2 = PG_SCAN2;
 
@@ -825,11 +828,22 @@ __global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* 
     if (u >= n) return;
     i64 a = off[u], b = off[u + 1];
     if (b - a < 2) return;     // a degree-1 vertex has only its tree edge
-    const int cnt = (int)(b - a < SCAN2 ? b - a : SCAN2);
+    const i64 deg = b - a;
+    const int cnt = (int)(deg < SCAN2 ? deg : SCAN2);
     uint2 fu = FL[u];
     uint2 fw[SCAN2];           // all loads issued before the first test
 #pragma unroll
-    for (int k = 0; k < SCAN2; ++k) fw[k] = k < cnt ? FL[(u32)tgt[a + k]] : fu;
+    for (int k = 0; k < SCAN2; ++k) {
+        // which slots: PG_SAMPLE2_MODE 0 = first, 1 = last, 2 = spread over the row
+#if PG_SAMPLE2_MODE == 1
+        const i64 s = b - 1 - k;
+#elif PG_SAMPLE2_MODE == 2
+        const i64 s = a + (deg * k) / SCAN2;
+#else
+        const i64 s = a + k;
+#endif
+        fw[k] = k < cnt ? FL[(u32)tgt[s]] : fu;
+    }
     int linked = 0;
 #pragma unroll
     for (int k = 0; k < SCAN2; ++k) {
