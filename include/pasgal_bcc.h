@@ -117,6 +117,13 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* Connected components (SPEC.md:413-420 `connected_components`): the
+ * spanning-forest stage of FAST-BCC on its own.  comp[v] = minimum vertex id of v's
+ * component (deterministic); *count (device int64) = number of components.  Uses the
+ * pasgal_bcc workspace.  Asynchronous. */
+int pasgal_cc(const pasgal_csr_t* g, uint32_t* comp, int64_t* count, void* workspace,
+              size_t workspace_bytes, uint64_t seed, void* stream);
+
 /* ---------------- device graph construction (north-star subsystem 1) ---------------- */
 
 /* Temp bytes for pasgal_csr_from_keys with `nkeys` keys on n vertices. */

@@ -54,6 +54,8 @@ def _load():
     lib.oracle_is_symmetric.restype = ctypes.c_int
     lib.oracle_canonical_min_eid.argtypes = [ctypes.c_int64, _i64p, _u32p, _i32p, ctypes.c_int64, _u32p]
     lib.oracle_canonical_min_eid.restype = ctypes.c_int
+    lib.oracle_connected_components.argtypes = [ctypes.c_int64, _i64p, _u32p, _i32p]
+    lib.oracle_connected_components.restype = ctypes.c_int64
     lib.oracle_count_upper.argtypes = [ctypes.c_int64, _i64p, _u32p]
     lib.oracle_count_upper.restype = ctypes.c_int64
     lib.host_csr_from_keys.argtypes = [ctypes.c_int64, _u64p, ctypes.c_int64, _i64p, _u32p]
@@ -140,6 +142,19 @@ def canonical_min_eid(offsets, targets, labels):
     if st != 0:
         raise MemoryError("oracle allocation failed")
     return out[: tgt.shape[0]]
+
+
+def connected_components(offsets, targets):
+    """Components labelled by their minimum vertex id (BFS in increasing start order);
+    restates SPEC.md:413-420 (the reference ships no code for it).  Returns (int32[n], count)."""
+    lib = _load()
+    off, tgt = _csr(offsets, targets)
+    n = off.shape[0] - 1
+    comp = np.empty(max(n, 1), dtype=np.int32)
+    c = lib.oracle_connected_components(n, _p(off, _i64p), _p(tgt, _u32p), _p(comp, _i32p))
+    if c < 0:
+        raise MemoryError("oracle allocation failed")
+    return comp[:n], int(c)
 
 
 def count_upper(offsets, targets):

@@ -227,3 +227,34 @@ int64_t oracle_count_upper(int64_t n, const int64_t* off, const uint32_t* tgt) {
         for (int64_t s = off[u]; s < off[u + 1]; ++s) c += (int64_t)tgt[s] > u;
     return c;
 }
+
+/* ------------------------------------------------------------------------- */
+/* connected components (SPEC.md:413-420 `connected_components`; the reference */
+/* ships no code for it): BFS from every unvisited vertex in increasing order, */
+/* so each component is labelled by its minimum vertex id.                     */
+/* ------------------------------------------------------------------------- */
+int64_t oracle_connected_components(int64_t n, const int64_t* off, const uint32_t* tgt, int32_t* comp) {
+    int32_t* queue = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    if (!queue) return -ORC_NOMEM;
+    for (int64_t v = 0; v < n; ++v) comp[v] = -1;
+    int64_t count = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        if (comp[r] != -1) continue;
+        ++count;
+        int64_t head = 0, tail = 0;
+        comp[r] = (int32_t)r;
+        queue[tail++] = (int32_t)r;
+        while (head < tail) {
+            int64_t u = queue[head++];
+            for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+                int64_t w = tgt[e];
+                if (comp[w] == -1) {
+                    comp[w] = (int32_t)r;
+                    queue[tail++] = (int32_t)w;
+                }
+            }
+        }
+    }
+    free(queue);
+    return count;
+}

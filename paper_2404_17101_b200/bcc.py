@@ -136,6 +136,40 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
     return out
 
 
+def connected_components_device(offsets, targets, *, seed=0, workspace=None):
+    """Connected components of a symmetric device CSR: returns
+    (comp int32 tensor [n] holding each vertex's component minimum id, count tensor)."""
+    lib = _lib.load()
+    offsets = offsets.contiguous()
+    targets = targets.contiguous()
+    n, m = offsets.shape[0] - 1, targets.shape[0]
+    dev = offsets.device
+    need = workspace_bytes(n, m)
+    ws = workspace if workspace is not None else _workspace(dev, need)
+    comp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    csr = _csr_struct(offsets, targets)
+    st = lib.pasgal_cc(ctypes.byref(csr), _vp(comp), _vp(count), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
+                       ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    _lib.check(st, "cc")
+    return comp[:n], count
+
+
+def connected_components(g, *, seed=0, validate=True, device="cuda"):
+    """Host form: (labels int64[n] = component minimum vertex id, component count)."""
+    if isinstance(g, DeviceGraph):
+        off_d, tgt_d = g.offsets, g.targets
+    else:
+        off_d = torch.from_numpy(np.ascontiguousarray(g.offsets, dtype=np.int64)).to(device)
+        tg = np.asarray(g.targets)
+        tg = tg.view(np.int32) if tg.dtype == np.uint32 else tg.astype(np.int32)
+        tgt_d = torch.from_numpy(np.ascontiguousarray(tg)).to(device)
+    if validate:
+        validate_device(off_d, tgt_d)
+    comp, count = connected_components_device(off_d, tgt_d, seed=seed)
+    return comp.cpu().numpy().astype(np.int64), int(count.item())
+
+
 def unpack_articulation(bits, n):
     """uint32 bitmap (bit v&31 of word v>>5) -> bool[n]."""
     b = np.ascontiguousarray(bits).view(np.uint8)

@@ -1280,6 +1280,52 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     return PASGAL_OK;
 }
 
+// ----------------------------------------------------------------------------
+// stand-alone connected components: S2 alone.  Union by
+// index makes every component's root its minimum vertex id, so the output is deterministic
+// and equal to a sequential labelling by minimum id.
+// ----------------------------------------------------------------------------
+__global__ void k_cc_out(i64 n, const u32* __restrict__ P, u32* comp, Ctr* ctr) {
+    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    u32 isroot = 0;
+    if (v < n) {
+        u32 r = P[v];
+        comp[v] = r;
+        isroot = r == (u32)v;
+    }
+    u32 cnt = __popc(__ballot_sync(0xFFFFFFFFu, isroot));
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr->ncomp, cnt);
+}
+
+__global__ void k_cc_count(const Ctr* ctr, i64* count) { *count = ctr->ncomp; }
+
+int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws_ptr, size_t ws_bytes, u64 seed,
+              cudaStream_t st) {
+    const i64 n = g->n;
+    Ws w;
+    size_t need = carve(w, nullptr, n, g->m_slots);
+    if (ws_bytes < need) return PASGAL_EWORKSPACE;
+    carve(w, (char*)ws_ptr, n, g->m_slots);
+    const i64* off = g->offsets;
+    const int32_t* tgt = g->targets;
+    const int B = 256;
+    PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
+    if (n > 0) {
+        k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C);
+        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB);
+        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB);
+        k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
+        k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
+        k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
+        k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
+        k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
+        k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
+    }
+    k_cc_count<<<1, 1, 0, st>>>(w.ctr, count_dev);
+    PG_LAUNCH_CHECK();
+    return PASGAL_OK;
+}
+
 size_t bcc_workspace_bytes(i64 n, i64 m) {
     Ws w;
     return carve(w, nullptr, n, m);

@@ -6,6 +6,8 @@ namespace pg {
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
                cudaStream_t st, pasgal_bcc_prof_t* prof);
 size_t bcc_workspace_bytes(i64 n, i64 m);
+int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
+              cudaStream_t st);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gen_grid_temp_bytes(i64 rows, i64 cols);
 int gen_grid(i64 rows, i64 cols, u64 seed, u64 thr, int keep_all, i64* off, int32_t* tgt, i64* m_dev, void* temp,
@@ -50,6 +52,15 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
 int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
                uint64_t seed, uint32_t flags, void* stream) {
     return pasgal_bcc_ex(g, out, workspace, workspace_bytes, seed, flags, stream, nullptr);
+}
+
+int pasgal_cc(const pasgal_csr_t* g, uint32_t* comp, int64_t* count, void* workspace, size_t workspace_bytes,
+              uint64_t seed, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!count || (g->n > 0 && !comp)) return PASGAL_EINVAL;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::cc_launch(g, comp, count, workspace, workspace_bytes, seed, (cudaStream_t)stream);
 }
 
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {

@@ -234,3 +234,16 @@ def test_repeated_calls_reuse_workspace():
         else:
             got = pg.canonical_edge_partition(pg.Graph(off, tgt), pg.BccLabels(art, cnt, edge_label=lab))
             assert np.array_equal(got, pg.min_eid_to_partition(pg.Graph(off, tgt), want)), it
+
+
+def test_connected_components_op():
+    """the stand-alone CC op equals the oracle labelling (component min id)."""
+    cases = golden_io.kats() + golden_io.corpus()[:120] + [golden_io.single(f) for f in golden_io.SINGLES]
+    for case in cases:
+        want, cnt = oracle.connected_components(case.offsets, case.targets)
+        got, gcnt = pg.connected_components(pg.Graph(case.offsets, case.targets))
+        assert gcnt == cnt and np.array_equal(got, want), case.name
+    for dg in [pg.make_config("c2"), pg.make_config("c3")]:
+        want, cnt = oracle.connected_components(dg.offsets.cpu().numpy(), dg.targets.cpu().numpy().view(np.uint32))
+        comp, count = pg.connected_components_device(dg.offsets, dg.targets)
+        assert int(count.item()) == cnt and np.array_equal(comp.cpu().numpy(), want)

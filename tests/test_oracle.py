@@ -99,3 +99,14 @@ def test_oracle_vs_live_reference_random():
         assert np.array_equal(r.edge_label, ref._edge_label)
         assert np.array_equal(r.articulation, ref.articulation)
         assert r.bcc_count == ref.bcc_count
+
+
+def test_oracle_connected_components_kats():
+    """two disjoint triangles -> 2 components; empty n=5 -> 5."""
+    kats = {c.name: c for c in golden_io.kats()}
+    comp, cnt = oracle.connected_components(kats["two_triangles"].offsets, kats["two_triangles"].targets)
+    assert cnt == 2 and comp.tolist() == [0, 0, 0, 3, 3, 3]
+    comp, cnt = oracle.connected_components(kats["empty5"].offsets, kats["empty5"].targets)
+    assert cnt == 5 and comp.tolist() == [0, 1, 2, 3, 4]
+    comp, cnt = oracle.connected_components(kats["isolated_plus_edge"].offsets, kats["isolated_plus_edge"].targets)
+    assert cnt == 3 and comp.tolist() == [0, 1, 1, 3]
