@@ -124,6 +124,16 @@ int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace
 int pasgal_cc(const pasgal_csr_t* g, uint32_t* comp, int64_t* count, void* workspace,
               size_t workspace_bytes, uint64_t seed, void* stream);
 
+/* Canonicaliser (results.py:91-112 canonical_edge_partition): relabels
+ * any per-slot labelling whose ids lie in [0, label_bound) so that every slot carries the
+ * minimum undirected edge id (rank of the u<v slot in CSR order) of its class; ids outside
+ * the bound (0xFFFFFFFF = unlabelled) pass through.  Two labellings describe the same
+ * partition iff their canonical forms are equal.  labels_out may alias labels_in.  Rows
+ * must be sorted.  Asynchronous. */
+size_t pasgal_canonicalize_temp_bytes(int64_t n, int64_t m_slots, int64_t label_bound);
+int pasgal_canonicalize(const pasgal_csr_t* g, const uint32_t* labels_in, int64_t label_bound,
+                        uint32_t* labels_out, void* temp, size_t temp_bytes, void* stream);
+
 /* ---------------- device graph construction (north-star subsystem 1) ---------------- */
 
 /* Temp bytes for pasgal_csr_from_keys with `nkeys` keys on n vertices. */

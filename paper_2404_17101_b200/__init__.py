@@ -8,13 +8,14 @@ CUDA kernels behind a C-ABI (include/pasgal_bcc.h).  See DESIGN.md.
 from .results import BccLabels, canonical_edge_partition, canonical_relabel, min_eid_to_partition
 from .graph import (CONFIGS, DeviceGraph, Graph, csr_from_keys, gen_grid, gen_knn, gen_rmat, make_config,
                     symmetrize_edges)
-from .bcc import (DeviceBcc, HostBuffers, connected_components, connected_components_device)
+from .bcc import (DeviceBcc, HostBuffers, canonicalize_device, connected_components, connected_components_device,
+                  same_partition_device)
 from .bcc import bcc, bcc_device, release_workspace, unpack_articulation, validate_device, workspace_bytes
 
 __all__ = [
     "BccLabels", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
     "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",
-    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
+    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonicalize_device", "same_partition_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
     "validate_device", "workspace_bytes",
 ]
 

@@ -57,6 +57,8 @@ SIGNATURES = {
     "pasgal_bcc_ex": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP,
                              ctypes.POINTER(PasgalBccProf)]),
     "pasgal_cc": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _VP, _VP, _SZ, _U64, _VP]),
+    "pasgal_canonicalize_temp_bytes": (_SZ, [_I64, _I64, _I64]),
+    "pasgal_canonicalize": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _I64, _VP, _VP, _SZ, _VP]),
     "pasgal_csr_validate": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
     "pasgal_csr_build_temp_bytes": (_SZ, [_I64, _I64]),
     "pasgal_csr_from_keys": (_INT, [_I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _SZ, _VP]),

@@ -170,6 +170,33 @@ def connected_components(g, *, seed=0, validate=True, device="cuda"):
     return comp.cpu().numpy().astype(np.int64), int(count.item())
 
 
+def canonicalize_device(offsets, targets, labels, label_bound=None):
+    """Device canonical form of any per-slot labelling (results.py:91-112 semantics): every
+    slot gets the minimum undirected edge id of its class.  ``labels``: int32/uint32 CUDA
+    tensor with ids in [0, label_bound) (default: max(n, M)); 0xFFFFFFFF passes through."""
+    lib = _lib.load()
+    offsets = offsets.contiguous()
+    targets = targets.contiguous()
+    n, m = offsets.shape[0] - 1, targets.shape[0]
+    bound = int(label_bound if label_bound is not None else max(n, m, 1))
+    lab = labels.contiguous().view(torch.int32)
+    out = torch.empty_like(lab)
+    tb = lib.pasgal_canonicalize_temp_bytes(n, m, bound)
+    temp = torch.empty(tb, dtype=torch.uint8, device=offsets.device)
+    csr = _csr_struct(offsets, targets)
+    st = lib.pasgal_canonicalize(ctypes.byref(csr), _vp(lab), bound, _vp(out), _vp(temp), tb,
+                                 ctypes.c_void_p(torch.cuda.current_stream(offsets.device).cuda_stream))
+    _lib.check(st, "canonicalize")
+    return out
+
+
+def same_partition_device(offsets, targets, labels_a, labels_b, label_bound=None):
+    """True iff two per-slot labellings induce the same edge partition (device comparator)."""
+    a = canonicalize_device(offsets, targets, labels_a, label_bound)
+    b = canonicalize_device(offsets, targets, labels_b, label_bound)
+    return bool(torch.equal(a, b))
+
+
 def unpack_articulation(bits, n):
     """uint32 bitmap (bit v&31 of word v>>5) -> bool[n]."""
     b = np.ascontiguousarray(bits).view(np.uint8)

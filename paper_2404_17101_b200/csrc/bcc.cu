@@ -154,11 +154,10 @@ __global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C) {
     HEAD[v] = PG_INV;
 }
 
-__global__ void k_canon_init(i64 n, u32* UCNT, u32* CANON) {
+__global__ void k_canon_init(i64 n, u32* UCNT, i64 nlab, u32* CANON) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    UCNT[v] = 0;
-    CANON[v] = PG_INV;
+    if (v < n) UCNT[v] = 0;
+    if (v < nlab) CANON[v] = PG_INV;
 }
 
 // Local phase (the paper's vertical granularity control recast for the GPU): a CTA owns a
@@ -1031,7 +1030,7 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_canon_count(const i64* __restrict
 __global__ void __launch_bounds__(WCH_BLOCK) k_canon_min(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                          i64 n, i64 m, const u32* __restrict__ crow,
                                                          const u32* __restrict__ UCNT, const u32* __restrict__ UOFF,
-                                                         const u32* __restrict__ label, u32* CANON) {
+                                                         const u32* __restrict__ label, i64 nlab, u32* CANON) {
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
@@ -1046,10 +1045,10 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_canon_min(const i64* __restrict__
         bool up = false;
         u32 lab = 0, eid = 0;
         if (valid && (u32)tgt[s] > row) {
-            up = true;
             // the row's upper part is its last UCNT slots (rows are sorted)
             eid = (u32)((i64)UOFF[row] + (s - (off[row + 1] - (i64)UCNT[row])));
             lab = label[s];
+            up = (i64)lab < nlab;   // ids outside [0, nlab) are not canonicalised
         }
         unsigned act = __ballot_sync(0xFFFFFFFFu, up);
         if (up) {
@@ -1060,11 +1059,11 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_canon_min(const i64* __restrict__
     }
 }
 
-__global__ void k_canon_apply(i64 m, const u32* __restrict__ CANON, u32* label) {
+__global__ void k_canon_apply(i64 m, const u32* __restrict__ CANON, i64 nlab, const u32* in, u32* out) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= m) return;
-    u32 l = label[s];
-    if (l != PG_INV) label[s] = CANON[l];
+    u32 l = in[s];
+    out[s] = (i64)l < nlab ? CANON[l] : l;
 }
 
 struct UcntLoad {
@@ -1264,14 +1263,14 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
     if (flags & PASGAL_BCC_CANONICAL) {
-        PG_K(k_canon_init<<<nblk(n, B), B, 0, st>>>(n, w.UCNT, w.CANON));
+        PG_K(k_canon_init<<<nblk(n, B), B, 0, st>>>(n, w.UCNT, n, w.CANON));
         if (w.nch > 0) PG_K(k_canon_count<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT));
         PG_CUDA_TRY(launch_scan<u32>(n, w.SCAN, 0u, SumOp(), UcntLoad{w.UCNT}, UoffStore{w.UOFF}, (u32*)nullptr, st));
         ++nl;
         if (w.nch > 0)
             PG_K(k_canon_min<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.UCNT, w.UOFF,
-                                                                   out->edge_label, w.CANON));
-        if (m > 0) PG_K(k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, out->edge_label));
+                                                                   out->edge_label, n, w.CANON));
+        if (m > 0) PG_K(k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, w.CANON, n, out->edge_label, out->edge_label));
         PG_LAUNCH_CHECK();
     }
     PG_CUDA_TRY(mark(PASGAL_STAGE_CANONICAL));
@@ -1322,6 +1321,59 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
         k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
     }
     k_cc_count<<<1, 1, 0, st>>>(w.ctr, count_dev);
+    PG_LAUNCH_CHECK();
+    return PASGAL_OK;
+}
+
+// ----------------------------------------------------------------------------
+// stand-alone canonicaliser (results.py:91-112): any per-slot labelling
+// with ids in [0, nlab) -> every slot labelled by the minimum undirected edge id of its
+// class.  Ids outside [0, nlab) (e.g. 0xFFFFFFFF = unlabelled) pass through unchanged.
+// ----------------------------------------------------------------------------
+struct CanonWs {
+    u32 *UCNT, *UOFF, *CANON, *CROW;
+    u64* SCAN;
+};
+static size_t canon_carve(CanonWs& c, char* base, i64 n, i64 m, i64 nlab) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) -> char* {
+        o = (o + 255) & ~(size_t)255;
+        char* p = base ? base + o : nullptr;
+        o += bytes;
+        return p;
+    };
+    i64 nn = n > 0 ? n : 1;
+    c.UCNT = (u32*)take(4 * nn);
+    c.UOFF = (u32*)take(4 * nn);
+    c.CANON = (u32*)take(4 * (nlab > 0 ? nlab : 1));
+    c.CROW = (u32*)take(4 * (num_chunks(m) + 1));
+    c.SCAN = (u64*)take(scan_status_bytes(nn));
+    return o + 256;
+}
+
+size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab) {
+    CanonWs c;
+    return canon_carve(c, nullptr, n, m, nlab);
+}
+
+int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
+                        cudaStream_t st) {
+    const i64 n = g->n, m = g->m_slots;
+    CanonWs c;
+    if (temp_bytes < canon_carve(c, nullptr, n, m, nlab)) return PASGAL_EWORKSPACE;
+    canon_carve(c, (char*)temp, n, m, nlab);
+    const int B = 256;
+    const i64 nch = num_chunks(m);
+    const i64* off = g->offsets;
+    const int32_t* tgt = g->targets;
+    if (n == 0 || m == 0) return PASGAL_OK;
+    i64 init = n > nlab ? n : nlab;
+    k_canon_init<<<nblk(init, B), B, 0, st>>>(n, c.UCNT, nlab, c.CANON);
+    k_chunk_rows<<<nblk(nch, B), B, 0, st>>>(off, n, m, nch, c.CROW);
+    k_canon_count<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, c.CROW, c.UCNT);
+    PG_CUDA_TRY(launch_scan<u32>(n, c.SCAN, 0u, SumOp(), UcntLoad{c.UCNT}, UoffStore{c.UOFF}, (u32*)nullptr, st));
+    k_canon_min<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, c.CROW, c.UCNT, c.UOFF, in, nlab, c.CANON);
+    k_canon_apply<<<nblk(m, B), B, 0, st>>>(m, c.CANON, nlab, in, out);
     PG_LAUNCH_CHECK();
     return PASGAL_OK;
 }

@@ -6,6 +6,9 @@ namespace pg {
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
                cudaStream_t st, pasgal_bcc_prof_t* prof);
 size_t bcc_workspace_bytes(i64 n, i64 m);
+size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
+int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
+                        cudaStream_t st);
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
               cudaStream_t st);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -61,6 +64,20 @@ int pasgal_cc(const pasgal_csr_t* g, uint32_t* comp, int64_t* count, void* works
     if (!count || (g->n > 0 && !comp)) return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
     return pg::cc_launch(g, comp, count, workspace, workspace_bytes, seed, (cudaStream_t)stream);
+}
+
+size_t pasgal_canonicalize_temp_bytes(int64_t n, int64_t m_slots, int64_t label_bound) {
+    return pg::canonicalize_temp_bytes(n < 0 ? 0 : n, m_slots < 0 ? 0 : m_slots, label_bound < 0 ? 0 : label_bound);
+}
+
+int pasgal_canonicalize(const pasgal_csr_t* g, const uint32_t* labels_in, int64_t label_bound, uint32_t* labels_out,
+                        void* temp, size_t temp_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (label_bound < 0 || label_bound > ((int64_t)1 << 32) || (g->m_slots > 0 && (!labels_in || !labels_out)))
+        return PASGAL_EINVAL;
+    if (!temp) return PASGAL_EWORKSPACE;
+    return pg::canonicalize_launch(g, labels_in, label_bound, labels_out, temp, temp_bytes, (cudaStream_t)stream);
 }
 
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {

@@ -247,3 +247,24 @@ def test_connected_components_op():
         want, cnt = oracle.connected_components(dg.offsets.cpu().numpy(), dg.targets.cpu().numpy().view(np.uint32))
         comp, count = pg.connected_components_device(dg.offsets, dg.targets)
         assert int(count.item()) == cnt and np.array_equal(comp.cpu().numpy(), want)
+
+
+def test_device_canonicaliser_and_comparator():
+    """the stand-alone device canonicaliser reproduces the oracle's
+    canonical form from the reference's raw labels, and the comparator tells partitions
+    apart."""
+    for case in golden_io.kats() + golden_io.corpus()[:60] + [golden_io.single(f) for f in golden_io.SINGLES]:
+        if case.m == 0:
+            continue
+        off, tgt = _dev(case)
+        ref_lab = torch.from_numpy(case.label.astype(np.int32)).cuda()   # reference raw labels (-1 = none)
+        got = pg.canonicalize_device(off, tgt, ref_lab).cpu().numpy().view(np.uint32)
+        want = oracle.canonical_min_eid(case.offsets, case.targets, case.label)
+        assert np.array_equal(got, want), case.name
+        r = pg.bcc_device(off, tgt)
+        assert pg.same_partition_device(off, tgt, r.edge_label, ref_lab), case.name
+    # a partition that differs (merge two BCCs of the path a-b-c) is detected
+    path = [c for c in golden_io.kats() if c.name == "path3"][0]
+    off, tgt = _dev(path)
+    lab = torch.from_numpy(path.label.astype(np.int32)).cuda()
+    assert not pg.same_partition_device(off, tgt, lab, torch.zeros_like(lab))
