@@ -134,6 +134,13 @@ size_t pasgal_canonicalize_temp_bytes(int64_t n, int64_t m_slots, int64_t label_
 int pasgal_canonicalize(const pasgal_csr_t* g, const uint32_t* labels_in, int64_t label_bound,
                         uint32_t* labels_out, void* temp, size_t temp_bytes, void* stream);
 
+/* Positioned error report for a loaded CSR (graph.py:380-395): host_out[0] = first index i
+ * with offsets[i-1] > offsets[i] (-1 if none), host_out[1] = first slot whose target lies
+ * outside [0, n) (-1 if none).  Used by the .bin loader to raise GraphFormatError with the
+ * reference's byte positions.  scratch16: 16 bytes of device memory.  SYNCHRONISES
+ * `stream`. */
+int pasgal_csr_first_error(const pasgal_csr_t* g, void* scratch16, int64_t* host_out, void* stream);
+
 /* ---------------- device graph construction (north-star subsystem 1) ---------------- */
 
 /* Temp bytes for pasgal_csr_from_keys with `nkeys` keys on n vertices. */

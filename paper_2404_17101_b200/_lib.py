@@ -59,6 +59,7 @@ SIGNATURES = {
     "pasgal_cc": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _VP, _VP, _SZ, _U64, _VP]),
     "pasgal_canonicalize_temp_bytes": (_SZ, [_I64, _I64, _I64]),
     "pasgal_canonicalize": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _I64, _VP, _VP, _SZ, _VP]),
+    "pasgal_csr_first_error": (_INT, [ctypes.POINTER(PasgalCsr), _VP, ctypes.POINTER(ctypes.c_int64), _VP]),
     "pasgal_csr_validate": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
     "pasgal_csr_build_temp_bytes": (_SZ, [_I64, _I64]),
     "pasgal_csr_from_keys": (_INT, [_I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _SZ, _VP]),

@@ -1378,6 +1378,31 @@ int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out
     return PASGAL_OK;
 }
 
+// first offending index of a CSR for positioned load errors (graph.py:380-395 semantics):
+// out[0] = first i with off[i] > off[i+1], out[1] = first slot with a target outside [0,n)
+__global__ void k_first_bad_offset(i64 n, const i64* __restrict__ off, unsigned long long* out) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && off[i] > off[i + 1]) atomicMin(out, (unsigned long long)(i + 1));
+}
+__global__ void k_first_bad_target(i64 n, i64 m, const int32_t* __restrict__ tgt, unsigned long long* out) {
+    i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < m && (tgt[s] < 0 || (i64)tgt[s] >= n)) atomicMin(out + 1, (unsigned long long)s);
+}
+int csr_first_error(const pasgal_csr_t* g, void* scratch, int64_t* host_out, cudaStream_t st) {
+    const i64 n = g->n, m = g->m_slots;
+    unsigned long long* d = (unsigned long long*)scratch;
+    PG_CUDA_TRY(cudaMemsetAsync(d, 0xFF, 2 * sizeof(unsigned long long), st));
+    const int B = 256;
+    if (n > 0) k_first_bad_offset<<<nblk(n, B), B, 0, st>>>(n, g->offsets, d);
+    if (m > 0) k_first_bad_target<<<nblk(m, B), B, 0, st>>>(n, m, g->targets, d);
+    unsigned long long h[2];
+    PG_CUDA_TRY(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaStreamSynchronize(st));
+    host_out[0] = h[0] == ~0ull ? -1 : (int64_t)h[0];
+    host_out[1] = h[1] == ~0ull ? -1 : (int64_t)h[1];
+    return PASGAL_OK;
+}
+
 size_t bcc_workspace_bytes(i64 n, i64 m) {
     Ws w;
     return carve(w, nullptr, n, m);

@@ -9,6 +9,7 @@ size_t bcc_workspace_bytes(i64 n, i64 m);
 size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
 int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
                         cudaStream_t st);
+int csr_first_error(const pasgal_csr_t* g, void* scratch, int64_t* host_out, cudaStream_t st);
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
               cudaStream_t st);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -64,6 +65,13 @@ int pasgal_cc(const pasgal_csr_t* g, uint32_t* comp, int64_t* count, void* works
     if (!count || (g->n > 0 && !comp)) return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
     return pg::cc_launch(g, comp, count, workspace, workspace_bytes, seed, (cudaStream_t)stream);
+}
+
+int pasgal_csr_first_error(const pasgal_csr_t* g, void* scratch16, int64_t* host_out, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!host_out || !scratch16) return PASGAL_EINVAL;
+    return pg::csr_first_error(g, scratch16, host_out, (cudaStream_t)stream);
 }
 
 size_t pasgal_canonicalize_temp_bytes(int64_t n, int64_t m_slots, int64_t label_bound) {

@@ -21,7 +21,7 @@ REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
 
-from pasgal.graph import Graph, from_edges, gen_grid, symmetrize  # noqa: E402
+from pasgal.graph import Graph, from_edges, gen_grid, save_bin, symmetrize  # noqa: E402
 from pasgal.oracles import bcc_hopcroft_tarjan  # noqa: E402
 from pasgal.results import canonical_edge_partition  # noqa: E402
 
@@ -154,6 +154,11 @@ def main():
     corp = [ref_case(g) for g in corpus()]
     np.savez_compressed(os.path.join(HERE, "corpus.npz"), **pack_cases(corp))
     print("corpus", len(corp), "graphs, slots", sum(c["targets"].shape[0] for c in corp))
+
+    # a binary graph file written by the reference's own save_bin (graph.py:398-409): the
+    # device loader must read it back identically
+    save_bin(kat["grid10x10"], os.path.join(HERE, "grid10x10_ref.bin"))
+    print("grid10x10_ref.bin written by pasgal.graph.save_bin")
 
     # BASELINE configs[0] (C1): grid 256x256, p=0.6, seed 1 -- CSR from the host twin of
     # the device generator, expected outputs from the reference oracle
