@@ -32,6 +32,12 @@
 namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
+#ifndef PG_TAGS_MINB
+#define PG_TAGS_MINB 1
+#endif
+#ifndef PG_LABELS_MINB
+#define PG_LABELS_MINB 1
+#endif
 #ifndef PG_NSAMPLE
 #define PG_NSAMPLE 2
 #endif
@@ -605,7 +611,7 @@ __device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u
 // in registers (warp-uniform), so a long row costs one atomic pair per 256-slot chunk
 // instead of one per window.  A row is stored without atomics when it begins and ends in
 // this chunk; a row that may extend into a neighbouring chunk uses atomics.
-__global__ void __launch_bounds__(WCH_BLOCK) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+__global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                     i64 n, i64 m, const u32* __restrict__ crow,
                                                     const u32* __restrict__ FIRST, uint2* W) {
     const int lane = threadIdx.x & 31;
@@ -949,7 +955,7 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
 // cross edge joins one component.  Most slots of a power-law graph point into the giant
 // component, so the target's component comes from the L2-resident membership bitmap and
 // only the remaining slots gather CIDV from HBM.
-__global__ void __launch_bounds__(WCH_BLOCK) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+__global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
                                                       const u32* __restrict__ CIDV, const u32* __restrict__ GBIT,
                                                       const Ctr* __restrict__ ctr, u32* label) {
