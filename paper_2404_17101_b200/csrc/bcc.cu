@@ -33,10 +33,10 @@ namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
 #ifndef PG_TAGS_MINB
-#define PG_TAGS_MINB 1
+#define PG_TAGS_MINB 8
 #endif
 #ifndef PG_LABELS_MINB
-#define PG_LABELS_MINB 1
+#define PG_LABELS_MINB 8
 #endif
 #ifndef PG_NSAMPLE
 #define PG_NSAMPLE 2
