@@ -14,7 +14,7 @@
 //   S2 First-CC   k_init, k_chunk_rows, k_cc_local (shared-memory union-find per id block),
 //                 k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
-//   S3 rooting    k_arc_link, root scan, k_arc_close, ruling-set list ranking (k_lr_walk1,
+//   S3 rooting    k_arc_link, k_arc_close (root chain, isolated slots), ruling-set list ranking (k_lr_walk1,
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
 //   S5 Last-CC    k_cc2_local / k_cc2_tree (non-fence tree edges, preorder blocks in shared
@@ -53,8 +53,9 @@ constexpr int GIANT_SAMPLES = 1024;
 constexpr int HEAVY_GRID = 148 * 4;
 
 struct Ctr {
-    u64 roots;    // packed root-scan total: (non-isolated roots << 31) | isolated vertices
-    u32 R;        // trees (roots) of the spanning forest, isolated vertices included
+    u32 r1;       // non-isolated roots (trees with >= 1 forest edge)
+    u32 niso;     // isolated vertices (no forest arc): preorder slots [0, niso)
+    u32 roothead; // 1 + down arc of the first root on the tour chain (0: empty; memset-safe)
     u32 giant;    // sampled largest component (First-CC)
     u32 giant2;   // sampled largest skeleton component (Last-CC)
     u32 ncomp;    // skeleton components
@@ -68,7 +69,7 @@ struct Ctr {
 // workspace carve-up (identical for sizing and use)
 // --------------------------------------------------------------------------
 struct Ws {
-    u32 *P, *HEAD, *RIDX, *ROOTS;
+    u32 *P, *HEAD;
     uint2* HAB;   // per vertex v: HAB[2v] = hook edge {a, b}; HAB[2v+1] = tour positions of arcs 2v, 2v+1
     u32* NEXT;
     u32 *SPLEN[2], *SPNEXT[2];
@@ -114,8 +115,6 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.P = (u32*)take(4 * nn);
     w.HAB = (uint2*)take(16 * nn);
     w.HEAD = (u32*)take(4 * nn);
-    w.RIDX = (u32*)take(4 * nn);
-    w.ROOTS = (u32*)take(4 * nn);
     w.NEXT = (u32*)take(4 * L);
     for (int b = 0; b < 2; ++b) {
         w.SPLEN[b] = (u32*)take(4 * w.ns);
@@ -156,7 +155,7 @@ __global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C) {
     if (v >= n) return;
     P[v] = (u32)v;
     C[v] = (u32)v;
-    HAB[2 * v] = make_uint2(PG_INV, PG_INV);
+    reinterpret_cast<uint4*>(HAB)[v] = make_uint4(PG_INV, PG_INV, 0u, 0u);   // whole 16-byte record
     HEAD[v] = PG_INV;
 }
 
@@ -322,8 +321,8 @@ __global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __re
 // virtual arcs: 2r = down into r, 2r+1 = up out of r.  Around every vertex the out-arcs
 // form a circular list NEXT (built with warp-aggregated atomicExch on HEAD[v]); the tour
 // successor is then uniformly succ(arc) = NEXT[arc^1].  A root's cycle is cut at its up
-// arc and consecutive non-isolated roots are chained, so the forest is one list headed by
-// the down arc of the first such root.  Isolated vertices (half of an RMAT graph) stay off
+// arc and the non-isolated roots are chained (in arbitrary order, by warp-aggregated
+// atomicExch on a global head), so the forest is one list headed by that chain's head.  Isolated vertices (half of an RMAT graph) stay off
 // the tour: the root scan gives them preorder slots [0, NISO) directly, and the tour's
 // vertices take [NISO, n).
 // --------------------------------------------------------------------------
@@ -368,74 +367,104 @@ __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32*
     arc_splice(NEXT, gb, arc_b, oldb);
 }
 
-// Close every out-arc list into a cycle (a root's cycle exits through its up arc) and set
-// the virtual arcs of non-isolated roots: succ(2r) = NEXT[2r+1] = first out-arc of r;
-// succ(2r+1) = NEXT[2r] = down arc of the next non-isolated root (or end of list).
+// Close every out-arc list into a cycle (a root's cycle exits through its up arc).  Roots:
+//   isolated (no forest arc): preorder slot f from a warp-aggregated counter, written here;
+//   otherwise succ(2r) = NEXT[2r+1] = first out-arc of r, and succ(2r+1) = NEXT[2r] = the
+//   down arc of the root chained before r (warp-aggregated atomicExch on ctr->roothead).
+// Neither the order of trees on the tour nor the order of isolated slots matters.
 constexpr u64 M31 = (1ull << 31) - 1;
 
-__global__ void k_arc_close(i64 n, const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
-                            const u32* __restrict__ P, const u32* __restrict__ RIDX,
-                            const u32* __restrict__ ROOTS, const Ctr* ctr, u32* NEXT) {
-    i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= n) return;
-    uint2 e = HAB[2 * x];
-    if (e.x != PG_INV) {
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-            u32 arc = 2 * (u32)x + d;
-            if (NEXT[arc] == PG_INV) {          // tail of the list of its source vertex
-                u32 src = d == 0 ? e.x : e.y;
-                NEXT[arc] = P[src] == src ? 2 * src + 1 : HEAD[src];
-            }
-        }
-    } else {
-        u32 r = (u32)x, h = HEAD[r];
-        if (h == PG_INV) return;               // isolated vertex: not on the tour
-        NEXT[2 * r + 1] = h;
-        u32 q = RIDX[r] + 1;
-        NEXT[2 * r] = q < (u32)(ctr->roots >> 31) ? 2 * ROOTS[q] : PG_INV;
-    }
-}
-
-// Root scan over vertices, packed two-field sum: (non-isolated root << 31) | isolated.
-// Non-isolated roots get their chain index; isolated vertices get their preorder slot.
-struct RootLoad {
-    const uint2* HAB;
-    const u32* HEAD;   // PG_INV: no forest arcs (isolated, or only self-loops)
-    __device__ __forceinline__ u64 operator()(i64 v) const {
-        if (HAB[2 * v].x != PG_INV) return 0;
-        return HEAD[v] == PG_INV ? 1ull : (1ull << 31);
-    }
-};
-struct RootStore {
-    u32 *RIDX, *ROOTS, *ROOTMARK;
+struct IsoOut {
     uint2* FL;
     u32 *FIRST, *PV, *E, *PPAR;
     uint2* W;
-    u32 *out_parent, *out_first;
-    __device__ __forceinline__ void operator()(i64 v, u64 ex, u64 val) const {
-        if (val >> 31) {
-            u32 k = (u32)(ex >> 31);
-            RIDX[v] = k;
-            ROOTS[k] = (u32)v;
-            ROOTMARK[v] = PG_INV;          // root articulation marker (k_artic)
-        } else if (val) {
-            u32 f = (u32)(ex & M31);
-            FL[v] = make_uint2(f, f);
-            FIRST[v] = f;
-            PV[f] = (u32)v;
-            E[f] = f;
-            PPAR[f] = (u32)v;
-            W[f] = make_uint2(f, f);
-            if (out_parent) out_parent[v] = (u32)v;
-            if (out_first) out_first[v] = f;
-        }
-    }
+    u32 *out_parent, *out_first, *ROOTMARK;
 };
 
-__global__ void k_roots_total(Ctr* ctr) {
-    u64 r = ctr->roots;
-    ctr->R = (u32)(r >> 31) + (u32)(r & M31);
+// One block = AC_B threads x AC_V vertices.  Both the isolated-slot counter and the root
+// chain are aggregated in shared memory first, so each block issues at most three global
+// atomics (a single global head hit once per warp serialised ~8M atomics at RMAT 2^28).
+constexpr int AC_B = 512, AC_V = 8;
+
+__global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restrict__ HAB,
+                                                    const u32* __restrict__ HEAD,
+                                                    const u32* __restrict__ P, Ctr* ctr,
+                                                    u32* NEXT, IsoOut io) {
+    __shared__ u32 s_niso, s_r1, s_head, s_tail, s_base;
+    if (threadIdx.x == 0) { s_niso = 0; s_r1 = 0; s_head = 0; s_tail = PG_INV; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const i64 base = (i64)blockIdx.x * (AC_B * AC_V) + threadIdx.x;
+    u32 slot[AC_V];
+#pragma unroll
+    for (int i = 0; i < AC_V; ++i) {
+        const i64 x = base + (i64)i * AC_B;
+        uint2 e = x < n ? HAB[2 * x] : make_uint2(0u, 0u);
+        const bool root = x < n && e.x == PG_INV;
+        const u32 h = root ? HEAD[x] : PG_INV;
+        const bool iso = root && h == PG_INV;
+        const bool chain = root && h != PG_INV;
+        if (x < n && !root) {
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                u32 arc = 2 * (u32)x + d;
+                if (NEXT[arc] == PG_INV) {          // tail of the list of its source vertex
+                    u32 src = d == 0 ? e.x : e.y;
+                    NEXT[arc] = P[src] == src ? 2 * src + 1 : HEAD[src];
+                }
+            }
+        }
+        // isolated vertices: block-local slot, made global after the block's one atomicAdd
+        const unsigned bi = __ballot_sync(0xFFFFFFFFu, iso);
+        u32 lb = 0;
+        if (bi && lane == __ffs(bi) - 1) lb = atomicAdd(&s_niso, (u32)__popc(bi));
+        lb = __shfl_sync(0xFFFFFFFFu, lb, bi ? __ffs(bi) - 1 : 0);
+        slot[i] = iso ? lb + (u32)__popc(bi & lt) : PG_INV;
+        // non-isolated roots: the warp's roots form a local chain spliced into the block chain
+        const unsigned bc = __ballot_sync(0xFFFFFFFFu, chain);
+        if (bc) {
+            const int lead = __ffs(bc) - 1;
+            u32 old = 0;
+            if (lane == lead) {
+                old = atomicExch(&s_head, 2 * (u32)x + 1);
+                atomicAdd(&s_r1, (u32)__popc(bc));
+            }
+            old = __shfl_sync(0xFFFFFFFFu, old, lead);
+            const unsigned later = bc & (lane == 31 ? 0u : (0xFFFFFFFEu << lane));
+            const u32 nxt = __shfl_sync(0xFFFFFFFFu, 2 * (u32)x, later ? __ffs(later) - 1 : lane);
+            if (chain) {
+                NEXT[2 * x + 1] = h;                  // down into r, then its first out-arc
+                if (later) NEXT[2 * x] = nxt;         // up out of r, then the next root's down arc
+                else if (old) NEXT[2 * x] = old - 1;
+                else s_tail = 2 * (u32)x;             // block tail: linked to the global chain
+                io.ROOTMARK[x] = PG_INV;              // root articulation marker (k_artic)
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_niso) s_base = atomicAdd(&ctr->niso, s_niso);
+        if (s_head) {
+            u32 old = atomicExch(&ctr->roothead, s_head);
+            NEXT[s_tail] = old - 1;                   // 0 - 1 = PG_INV ends the tour
+            atomicAdd(&ctr->r1, s_r1);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < AC_V; ++i) {
+        if (slot[i] == PG_INV) continue;
+        const u32 v = (u32)(base + (i64)i * AC_B), f = s_base + slot[i];
+        io.FL[v] = make_uint2(f, f);
+        io.FIRST[v] = f;
+        io.PV[f] = v;
+        io.E[f] = f;
+        io.PPAR[f] = v;
+        io.W[f] = make_uint2(f, f);
+        if (io.out_parent) io.out_parent[v] = v;
+        if (io.out_first) io.out_first[v] = f;
+    }
 }
 
 // ruling-set list ranking over succ(a) = NEXT[a^1].  Rulers: every on-tour arc a with
@@ -445,11 +474,10 @@ struct TourInfo {
     u32 head;     // first arc of the list, PG_INV if the tour is empty
     u32 len;      // arcs on the tour = 2 * (n - isolated)
 };
-__device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, const u32* ROOTS, i64 n) {
-    u64 r = ctr->roots;
+__device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, i64 n) {
     TourInfo t;
-    t.head = (r >> 31) ? 2 * ROOTS[0] : PG_INV;
-    t.len = (u32)(2 * (n - (i64)(r & M31)));
+    t.head = ctr->roothead - 1;                // PG_INV when no root is chained
+    t.len = (u32)(2 * (n - (i64)ctr->niso));
     return t;
 }
 __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, const uint2* HAB, const u32* HEAD,
@@ -464,11 +492,11 @@ __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, c
 }
 
 __global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
-                           const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr, u32* SPLEN,
+                           const u32* __restrict__ HEAD, const Ctr* ctr, u32* SPLEN,
                            u32* SPNEXT) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    const TourInfo t = tour_info(ctr, ROOTS, n);
+    const TourInfo t = tour_info(ctr, n);
     const i64 nsk = ns - 1;
     u32 x;
     if (!ruler_start(s, nsk, t, HAB, HEAD, x)) {
@@ -501,11 +529,11 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
 }
 
 __global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
-                           const u32* __restrict__ HEAD, const u32* __restrict__ ROOTS, const Ctr* ctr,
+                           const u32* __restrict__ HEAD, const Ctr* ctr,
                            const u32* __restrict__ SUFFIX, uint2* HABW, u32* TA) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
-    const TourInfo t = tour_info(ctr, ROOTS, n);
+    const TourInfo t = tour_info(ctr, n);
     u32 x;
     if (!ruler_start(s, ns - 1, t, HAB, HEAD, x)) return;
     u32 pos = t.len - SUFFIX[s];
@@ -533,7 +561,7 @@ struct PreLoad {
     // all reads are read-only for the kernel (__ldg), so the compiler may issue the next
     // items' gathers before this item's stores
     __device__ __forceinline__ u32 operator()(i64 k) const {
-        if (k >= 2 * (n - (i64)(ctr->roots & M31))) return 0u;
+        if (k >= 2 * (n - (i64)ctr->niso)) return 0u;
         u32 x = __ldg(TA + k);
         // one 16-byte record: the hook edge and both arcs' positions
         uint4 r = __ldg(reinterpret_cast<const uint4*>(HAB + 2 * (i64)(x >> 1)));
@@ -563,7 +591,7 @@ struct PreStore {
     u32 *out_parent, *out_first;
     __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
         if (!down) return;
-        f += (u32)(ctr->roots & M31);     // isolated vertices occupy [0, NISO)
+        f += ctr->niso;                   // isolated vertices occupy [0, niso)
         u64 t = T[k];
         u32 pt = (u32)(t >> 32), lo = (u32)t;
         u32 v = lo & ~VFLAG;
@@ -1002,7 +1030,10 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
     }
 }
 
-__global__ void k_finish(const Ctr* ctr, i64* bcc_count) { *bcc_count = (i64)ctr->ncomp - (i64)ctr->R; }
+// every tree root (isolated vertices included) is a singleton skeleton component
+__global__ void k_finish(const Ctr* ctr, i64* bcc_count) {
+    *bcc_count = (i64)ctr->ncomp - (i64)ctr->r1 - (i64)ctr->niso;
+}
 
 // --------------------------------------------------------------------------
 // canonical labels: min undirected edge id per BCC (results.py:103-112 equivalent)
@@ -1211,24 +1242,20 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
     PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
-    PG_CUDA_TRY(launch_scan<u64>(n, w.SCAN, 0ull, SumOp(), RootLoad{w.HAB, w.HEAD},
-                                 RootStore{w.RIDX, w.ROOTS, w.ROOTMARK, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent,
-                                           out->first},
-                                 &w.ctr->roots, st));
-    PG_K(k_roots_total<<<1, 1, 0, st>>>(w.ctr));
-    ++nl;
-    PG_K(k_arc_close<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.P, w.RIDX, w.ROOTS, w.ctr, w.NEXT));
+    PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
+        n, w.HAB, w.HEAD, w.P, w.ctr, w.NEXT,
+        IsoOut{w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first, w.ROOTMARK}));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
-    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[0],
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[0],
                                                      w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
         PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ROOTS, w.ctr, w.SPLEN[cur],
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[cur],
                                                      w.HAB, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
