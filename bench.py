@@ -476,13 +476,13 @@ def run_e2e(args, dg, dev, n, m):
         res = pg.bcc(g, device=dev, host_out=hb)
     dt = (time.perf_counter() - t0) / steps
     h2d = 8 * (n + 1) + 4 * m
-    d2h = 4 * m + 4 * ((n + 31) // 32) + 8
+    d2h = 4 * m + n + 8
     del res
     return {"value": (m // 2) / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps,
             "h2d_ms": round(h2d_s * 1e3, 1), "validate_ms": round(val_s * 1e3, 1),
             "path": "paper_2404_17101_b200.bcc(g) with host numpy CSR (pinned) -> H2D, validate, FAST-BCC, "
-                    "D2H labels+bitmap+count (pinned)"}
+                    "D2H labels+articulation bytes+count (pinned)"}
 
 
 def main():

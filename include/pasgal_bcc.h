@@ -71,8 +71,8 @@ typedef struct {
     uint32_t* first;
 } pasgal_bcc_out_t;
 
-/* Workspace for pasgal_bcc / pasgal_csr_validate: O(n) words plus one 4-byte row index
- * per 256-slot warp chunk ("O(n) auxiliary space"). */
+/* Workspace for pasgal_bcc (and pasgal_cc): O(n) words plus one 4-byte row index per
+ * 256-slot warp chunk ("O(n) auxiliary space"). */
 size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots);
 
 /* FAST-BCC on a symmetric, simple CSR with sorted rows.  Asynchronous.  Input is not
@@ -113,9 +113,15 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
  * the slot multiset closed under reversal (the k-th copy of w in row u has a k-th copy of
  * u in row w).  Parallel edges are BCC-legal as in the reference (twin pairing); a
  * self-loop slot is left unlabelled (0xFFFFFFFF), as the reference leaves it at -1.
- * SYNCHRONISES `stream`; returns the status (PASGAL_OK, _ERANGE, _EUNSORTED, _ENOTSYM). */
+ * SYNCHRONISES `stream`; returns the status (PASGAL_OK, _ERANGE, _EUNSORTED, _ENOTSYM).
+ * `workspace` >= pasgal_csr_validate_workspace_bytes(n, m_slots). */
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes,
                         void* stream);
+
+/* Workspace for pasgal_csr_validate: 4 bytes per slot (one bucketed 8-byte key per run of
+ * "up" slots, at most m/2 of them) plus ~8 KB per CTA of histograms -- O(m), like the
+ * reference's twin array (oracles.py:107-116).  May alias pasgal_bcc's workspace. */
+size_t pasgal_csr_validate_workspace_bytes(int64_t n, int64_t m_slots);
 
 /* Connected components (SPEC.md:413-420 `connected_components`): the
  * spanning-forest stage of FAST-BCC on its own.  comp[v] = minimum vertex id of v's
@@ -181,6 +187,11 @@ int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t*
                         int64_t* nkeys_dev, void* temp, size_t temp_bytes, void* stream);
 
 /* Human-readable status text. */
+/* Articulation bitmap -> one byte per vertex (0/1), on the device: the reference's
+ * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.
+ * Asynchronous on `stream`. */
+int pasgal_bits_to_bytes(const uint32_t* bits, int64_t n, uint8_t* bytes, void* stream);
+
 const char* pasgal_strerror(int status);
 
 /* Library version string. */

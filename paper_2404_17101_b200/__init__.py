@@ -10,7 +10,7 @@ from .graph import (CONFIGS, DeviceGraph, Graph, csr_from_keys, gen_grid, gen_kn
                     symmetrize_edges)
 from .bcc import (DeviceBcc, HostBuffers, canonicalize_device, connected_components, connected_components_device,
                   same_partition_device)
-from .bcc import bcc, bcc_device, release_workspace, unpack_articulation, validate_device, workspace_bytes
+from .bcc import articulation_bytes_device, bcc, bcc_device, release_workspace, unpack_articulation, validate_device, validate_workspace_bytes, workspace_bytes
 
 from .io import GraphFormatError, load_bin, save_bin
 
@@ -18,8 +18,8 @@ __all__ = [
     "GraphFormatError", "load_bin", "save_bin",
     "BccLabels", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
     "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",
-    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonicalize_device", "same_partition_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
-    "validate_device", "workspace_bytes",
+    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonicalize_device", "same_partition_device", "articulation_bytes_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
+    "validate_device", "validate_workspace_bytes", "workspace_bytes",
 ]
 
 __version__ = "0.1.0"

@@ -53,6 +53,7 @@ _SZ = ctypes.c_size_t
 # name -> (restype, argtypes); must match include/pasgal_bcc.h exactly
 SIGNATURES = {
     "pasgal_bcc_workspace_bytes": (_SZ, [_I64, _I64]),
+    "pasgal_csr_validate_workspace_bytes": (_SZ, [_I64, _I64]),
     "pasgal_bcc": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP]),
     "pasgal_bcc_ex": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP,
                              ctypes.POINTER(PasgalBccProf)]),
@@ -68,6 +69,7 @@ SIGNATURES = {
     "pasgal_gen_rmat_keys": (_INT, [_INT, _I64, _U64, _U32, _U32, _U32, _VP, _VP, _VP]),
     "pasgal_gen_knn_temp_bytes": (_SZ, [_I64, _INT]),
     "pasgal_gen_knn_keys": (_INT, [_I64, _INT, _U64, _INT, _VP, _VP, _VP, _SZ, _VP]),
+    "pasgal_bits_to_bytes": (_INT, [_VP, _I64, _VP, _VP]),
     "pasgal_strerror": (ctypes.c_char_p, [_INT]),
     "pasgal_version": (ctypes.c_char_p, []),
 }

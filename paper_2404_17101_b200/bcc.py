@@ -31,6 +31,10 @@ def workspace_bytes(n, m):
     return int(_lib.load().pasgal_bcc_workspace_bytes(int(n), int(m)))
 
 
+def validate_workspace_bytes(n, m):
+    return int(_lib.load().pasgal_csr_validate_workspace_bytes(int(n), int(m)))
+
+
 def _workspace(device, nbytes):
     """A cached device workspace of at least nbytes (the library never allocates)."""
     key = torch.device(device)
@@ -67,11 +71,13 @@ def _csr_struct(offsets, targets):
 
 def validate_device(offsets, targets, workspace=None):
     """Device check of the BCC preconditions (symmetric, sorted rows, ids in range).
-    Synchronises; raises ValueError like the reference (oracles.py:127-128)."""
+    Synchronises; raises ValueError like the reference (oracles.py:127-128).  A given
+    ``workspace`` smaller than ``validate_workspace_bytes(n, m)`` is replaced by the cached
+    one (validation needs O(m) scratch, the BCC workspace only O(n))."""
     lib = _lib.load()
     n, m = offsets.shape[0] - 1, targets.shape[0]
-    need = workspace_bytes(n, m)
-    ws = workspace if workspace is not None else _workspace(offsets.device, need)
+    need = validate_workspace_bytes(n, m)
+    ws = workspace if workspace is not None and workspace.numel() >= need else _workspace(offsets.device, need)
     csr = _csr_struct(offsets, targets)
     st = lib.pasgal_csr_validate(ctypes.byref(csr), _vp(ws), ws.numel(),
                                  ctypes.c_void_p(torch.cuda.current_stream(offsets.device).cuda_stream))
@@ -97,6 +103,8 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
     n, m = offsets.shape[0] - 1, targets.shape[0]
     dev = offsets.device
     need = workspace_bytes(n, m)
+    if validate and workspace is None:
+        need = max(need, validate_workspace_bytes(n, m))   # one cached buffer serves both
     ws = workspace if workspace is not None else _workspace(dev, need)
     if ws.numel() < need:
         raise ValueError("workspace too small")
@@ -203,18 +211,28 @@ def unpack_articulation(bits, n):
     return np.unpackbits(b, bitorder="little")[:n].astype(bool)
 
 
+def articulation_bytes_device(bits, n):
+    """Device uint32 bitmap -> device uint8[n] (0/1), by the library's kernel."""
+    out = torch.empty(max(n, 1), dtype=torch.uint8, device=bits.device)
+    st = _lib.load().pasgal_bits_to_bytes(_vp(bits), int(n), _vp(out),
+                                          ctypes.c_void_p(torch.cuda.current_stream(bits.device).cuda_stream))
+    _lib.check(st, "bits_to_bytes")
+    return out[:n]
+
+
 @dataclass
 class HostBuffers:
     """Optional caller-owned (ideally pinned) host buffers for ``bcc(..., host_out=)``:
-    labels are copied straight into them and the returned BccLabels views them."""
+    labels and articulation flags are copied straight into them and the returned
+    BccLabels views them (no host-side copy or unpack)."""
 
     edge_label: torch.Tensor    # int32 [>= M], cpu (pinned)
-    artic_bits: torch.Tensor    # int32 [>= ceil(n/32)], cpu (pinned)
+    articulation: torch.Tensor  # uint8 [>= n], cpu (pinned)
 
     @staticmethod
     def allocate(n, m, pinned=True):
         return HostBuffers(torch.empty(max(m, 1), dtype=torch.int32, pin_memory=pinned),
-                           torch.empty(max((n + 31) // 32, 1), dtype=torch.int32, pin_memory=pinned))
+                           torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=pinned))
 
 
 def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False, host_out=None):
@@ -246,18 +264,17 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
     n = off_d.shape[0] - 1
     m = tgt_d.shape[0]
     r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest)
+    art_d = articulation_bytes_device(r.artic_bits, n)
     if host_out is not None:
         host_out.edge_label[:m].copy_(r.edge_label, non_blocking=True)
-        nb = (n + 31) // 32
-        host_out.artic_bits[:nb].copy_(r.artic_bits, non_blocking=True)
+        host_out.articulation[:n].copy_(art_d, non_blocking=True)
         count = int(r.bcc_count.item())     # synchronises the stream
         lab = host_out.edge_label[:m].numpy().view(np.uint32)
-        bits = host_out.artic_bits[:nb].numpy()
+        art = host_out.articulation[:n].numpy().view(np.bool_)
     else:
         lab = r.edge_label.cpu().numpy().view(np.uint32)
-        bits = r.artic_bits.cpu().numpy()
+        art = art_d.cpu().numpy().view(np.bool_)
         count = int(r.bcc_count.item())
-    art = unpack_articulation(bits, n)
     if forest:
         return BccLabels(art, count, edge_label=lab,
                          comp=r.comp.cpu().numpy().astype(np.int64),

@@ -1135,49 +1135,166 @@ __device__ __forceinline__ i64 lower_bound_row(const int32_t* tgt, i64 a, i64 b,
     return a;
 }
 
-// Exact multiset symmetry with half the searches: every slot u->w with u < w must find its
-// own copy of u in row w (the k-th copy of w in row u pairs with the k-th copy of u in row
-// w: an injection from "up" slots to "down" slots), and the numbers of up and down slots
-// must be equal, which makes the injection a bijection.  The search runs in row w, the
-// larger id -- rarely a hub row in power-law graphs, whose hubs have small ids.
-__global__ void __launch_bounds__(WCH_BLOCK) k_validate_slots(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                              i64 n, i64 m, const u32* __restrict__ crow, Ctr* ctr,
-                                                              unsigned long long* updown) {
+// Exact multiset symmetry, bucketed so that every search is cache-local.
+//
+// Slots split into "up" (u -> w, w > u), "down" (w < u) and self-loops.  A maximal run of c
+// equal up slots u -> w in row u becomes one key (w, u, c > 1); the graph is symmetric iff
+// every key finds exactly c copies of u in row w and #up == #down (runs are distinct pairs,
+// so the key -> run map is injective on down slots, and equal counts make it onto).
+//   k_val_pass<false>  streams the CSR: range / order checks, up & down counts, and a
+//                      per-block histogram of the keys' bucket (w >> shift, VAL_BINS);
+//   (host)             rejects #up != #down before any key is written (so keys <= m/2);
+//   launch_scan        bucket-major exclusive scan of the histograms -> per-block bases;
+//   k_val_pass<true>   re-streams the same chunks and scatters the keys into buckets;
+//   k_val_check        walks the keys bucket by bucket, so the rows it searches (a
+//                      1/VAL_BINS slice of the id range) stay resident in L2.
+// The first version searched row w straight from the slot pass: ~17 DRAM sectors per
+// search on RMAT 2^28 (ncu: 1.17 TB read, 291 ms); searching the shorter row instead
+// still took 246 ms, because every slot then gathers the other row's offsets.
+constexpr int VAL_BINS_LB = 10, VAL_BINS = 1 << VAL_BINS_LB;
+constexpr int VAL_GRID = 148 * 8;
+constexpr u64 VAL_DUP = 1ull << 63;
+
+template <bool SCATTER>
+__global__ void __launch_bounds__(WCH_BLOCK) k_val_pass(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+                                                        i64 n, i64 m, const u32* __restrict__ crow, int shift,
+                                                        Ctr* ctr, unsigned long long* cnt, u32* hist,
+                                                        const u32* __restrict__ base, u64* __restrict__ keys) {
+    __shared__ u32 s_bin[VAL_BINS];
+    for (int i = threadIdx.x; i < VAL_BINS; i += WCH_BLOCK)
+        s_bin[i] = SCATTER ? base[(i64)i * gridDim.x + blockIdx.x] : 0u;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
-    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
-    if (c >= num_chunks(m)) return;
-    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
-    u32 cur = crow[c];
-    u32 err = 0, nup = 0, ndown = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    const i64 nch = num_chunks(m);
+    const i64 stride = (i64)gridDim.x * (WCH_BLOCK / 32);
+    u32 err = 0, nup = 0, ndown = 0, nkey = 0;
 #pragma unroll 1
-    for (i64 sb = s0; sb < s1; sb += 32) {
-        const i64 s = sb + lane;
-        const bool valid = s < s1;
-        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
-        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
-        if (!valid) continue;
-        const i64 u = row;
-        int32_t w = tgt[s];
-        if (w < 0 || (i64)w >= n) { err |= VERR_RANGE; continue; }
-        i64 re = off[u + 1];
-        if (s + 1 < re && tgt[s + 1] < w) { err |= VERR_UNSORTED; continue; }
-        if ((i64)w < u) { ++ndown; continue; }
-        if ((i64)w == u) continue;   // self-loop: its own reverse
-        ++nup;
-        i64 rs = off[u], k = 0;
-        while (s - k - 1 >= rs && tgt[s - k - 1] == w) ++k;   // copy index of w in row u
-        i64 ws = off[w], we = off[w + 1];
-        i64 q = lower_bound_row(tgt, ws, we, (int32_t)u) + k;
-        if (q >= we || tgt[q] != (int32_t)u) err |= VERR_NOTSYM;
+    for (i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5; c < nch; c += stride) {
+        const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+        u32 cur = crow[c];
+#pragma unroll 1
+        for (i64 sb = s0; sb < s1; sb += 32) {
+            const i64 s = sb + lane;
+            const bool valid = s < s1;
+            const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
+            cur = __shfl_sync(0xFFFFFFFFu, row, 31);
+            bool key = false;
+            u32 bin = PG_INV;
+            u64 kv = 0;
+            if (valid) {
+                const i64 u = row;
+                const int32_t w = tgt[s];
+                if (!SCATTER && (w < 0 || (i64)w >= n)) {
+                    err |= VERR_RANGE;
+                } else {
+                    const i64 rs = off[u], re = off[u + 1];
+                    if (!SCATTER && s + 1 < re && tgt[s + 1] < w) err |= VERR_UNSORTED;
+                    if ((i64)w > u) {
+                        ++nup;
+                        if (s == rs || tgt[s - 1] != w) {            // first slot of its run
+                            key = true;
+                            bin = (u32)w >> shift;
+                            const bool dup = s + 1 < re && tgt[s + 1] == w;
+                            kv = (dup ? VAL_DUP : 0ull) | ((u64)(u32)w << 32) | (u64)(u32)u;
+                        }
+                    } else if ((i64)w < u) {
+                        ++ndown;
+                    }
+                }
+            }
+            if (__ballot_sync(0xFFFFFFFFu, key)) {
+                const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);   // key lanes by bucket
+                if (key) {
+                    ++nkey;
+                    const int leader = __ffs(peers) - 1;
+                    u32 b0 = 0;
+                    if (lane == leader) b0 = atomicAdd(&s_bin[bin], (u32)__popc(peers));
+                    if (SCATTER) {
+                        b0 = __shfl_sync(peers, b0, leader);
+                        keys[b0 + (u32)__popc(peers & lt)] = kv;
+                    }
+                }
+            }
+        }
     }
-    err = __reduce_or_sync(0xFFFFFFFFu, err);
-    nup = __reduce_add_sync(0xFFFFFFFFu, nup);
-    ndown = __reduce_add_sync(0xFFFFFFFFu, ndown);
-    if (lane == 0) {
-        if (err) atomicOr(&ctr->verr, err);
-        if (nup) atomicAdd(updown, (unsigned long long)nup);
-        if (ndown) atomicAdd(updown + 1, (unsigned long long)ndown);
+    if (!SCATTER) {
+        err = __reduce_or_sync(0xFFFFFFFFu, err);
+        nup = __reduce_add_sync(0xFFFFFFFFu, nup);
+        ndown = __reduce_add_sync(0xFFFFFFFFu, ndown);
+        nkey = __reduce_add_sync(0xFFFFFFFFu, nkey);
+        if (lane == 0) {
+            if (err) atomicOr(&ctr->verr, err);
+            if (nup) atomicAdd(cnt, (unsigned long long)nup);
+            if (ndown) atomicAdd(cnt + 1, (unsigned long long)ndown);
+            if (nkey) atomicAdd(cnt + 2, (unsigned long long)nkey);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < VAL_BINS; i += WCH_BLOCK) hist[(i64)i * gridDim.x + blockIdx.x] = s_bin[i];
     }
+}
+
+struct ValHistLoad {
+    const u32* h;
+    __device__ __forceinline__ u32 operator()(i64 i) const { return h[i]; }
+};
+struct ValBaseStore {
+    u32* b;
+    __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { b[i] = ex; }
+};
+
+// One key per thread: row w must hold exactly c copies of u (c = 1 unless the key is
+// flagged, then c is re-counted in row u).
+__global__ void k_val_check(const i64* __restrict__ off, const int32_t* __restrict__ tgt, const u64* __restrict__ keys,
+                            i64 nkeys, Ctr* ctr) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nkeys) return;
+    const u64 kv = keys[i];
+    const int32_t u = (int32_t)(u32)kv, w = (int32_t)((u32)(kv >> 32) & 0x7FFFFFFFu);
+    const i64 ws = off[w], we = off[(i64)w + 1];
+    const i64 q = lower_bound_row(tgt, ws, we, u);
+    i64 c = 1;
+    if (kv & VAL_DUP) {
+        const i64 rs = off[u], re = off[(i64)u + 1];
+        i64 p = lower_bound_row(tgt, rs, re, w);
+        c = 0;
+        while (p + c < re && tgt[p + c] == w) ++c;
+    }
+    bool bad = q + c > we || (q + c < we && tgt[q + c] == u);
+    for (i64 j = 0; j < c && !bad; ++j) bad = tgt[q + j] != u;
+    if (bad) atomicOr(&ctr->verr, VERR_NOTSYM);
+}
+
+static inline unsigned val_grid(i64 m) {
+    unsigned b = chunk_blocks(m);
+    return b < (unsigned)VAL_GRID ? b : (unsigned)VAL_GRID;
+}
+
+struct ValWs {
+    Ctr* ctr;
+    unsigned long long* cnt;   // up, down, keys
+    u32 *CROW, *HIST, *BASE;
+    u64 *SCAN, *KEYS;
+};
+
+static size_t carve_val(ValWs& v, char* base, i64 n, i64 m) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) -> char* {
+        o = (o + 255) & ~(size_t)255;
+        char* p = base ? base + o : nullptr;
+        o += bytes;
+        return p;
+    };
+    (void)n;
+    const i64 nh = (i64)VAL_BINS * val_grid(m);
+    v.ctr = (Ctr*)take(sizeof(Ctr));
+    v.cnt = (unsigned long long*)take(4 * sizeof(unsigned long long));
+    v.CROW = (u32*)take(4 * (num_chunks(m) + 1));
+    v.HIST = (u32*)take(4 * nh);
+    v.BASE = (u32*)take(4 * nh);
+    v.SCAN = (u64*)take(scan_status_bytes(nh));
+    v.KEYS = (u64*)take(8 * (size_t)(m / 2 > 0 ? m / 2 : 1));   // keys <= #up == #down <= m/2
+    return o + 256;
 }
 
 // --------------------------------------------------------------------------
@@ -1441,31 +1558,85 @@ size_t bcc_workspace_bytes(i64 n, i64 m) {
     return carve(w, nullptr, n, m);
 }
 
+size_t validate_workspace_bytes(i64 n, i64 m) {
+    ValWs v;
+    return carve_val(v, nullptr, n, m);
+}
+
+// bitmap word k -> bytes [32k, 32k+32) (0/1), two 16-byte stores per thread; the tail word
+// writes only its n - 32k valid bytes.
+__global__ void k_bits_to_bytes(const u32* __restrict__ bits, i64 n, uint8_t* __restrict__ out) {
+    const i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 b0 = k * 32;
+    if (b0 >= n) return;
+    const u32 x = bits[k];
+    if (b0 + 32 <= n && ((uintptr_t)out & 15) == 0) {
+        u32 wv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const u32 nib = (x >> (4 * j)) & 0xFu;
+            wv[j] = (nib & 1u) | ((nib >> 1 & 1u) << 8) | ((nib >> 2 & 1u) << 16) | ((nib >> 3 & 1u) << 24);
+        }
+        uint4* o = reinterpret_cast<uint4*>(out + b0);
+        o[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        o[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    } else {
+        for (int j = 0; j < 32 && b0 + j < n; ++j) out[b0 + j] = (uint8_t)(x >> j & 1u);
+    }
+}
+
+int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st) {
+    if (n <= 0) return PASGAL_OK;
+    const i64 words = cdiv(n, 32);
+    k_bits_to_bytes<<<nblk(words, 256), 256, 0, st>>>(bits, n, out);
+    PG_LAUNCH_CHECK();
+    return PASGAL_OK;
+}
+
 int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
     const i64 n = g->n, m = g->m_slots;
-    Ws w;
-    size_t need = carve(w, nullptr, n, m);
+    ValWs v;
+    size_t need = carve_val(v, nullptr, n, m);
     if (ws_bytes < need) return PASGAL_EWORKSPACE;
-    carve(w, (char*)ws_ptr, n, m);
-    PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
+    carve_val(v, (char*)ws_ptr, n, m);
+    PG_CUDA_TRY(cudaMemsetAsync(v.ctr, 0, sizeof(Ctr), st));
+    PG_CUDA_TRY(cudaMemsetAsync(v.cnt, 0, 4 * sizeof(unsigned long long), st));
     const int B = 256;
-    k_validate_offsets<<<nblk(n + 1, B), B, 0, st>>>(n, m, g->offsets, w.ctr);
+    k_validate_offsets<<<nblk(n + 1, B), B, 0, st>>>(n, m, g->offsets, v.ctr);
     PG_LAUNCH_CHECK();
     Ctr h;
-    PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
     PG_CUDA_TRY(cudaStreamSynchronize(st));
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (m > 0 && n > 0) {
-        unsigned long long* updown = (unsigned long long*)w.SCAN;   // scratch: 2 counters
-        PG_CUDA_TRY(cudaMemsetAsync(updown, 0, 2 * sizeof(unsigned long long), st));
-        k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(g->offsets, n, m, w.nch, w.CROW);
-        k_validate_slots<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, w.CROW, w.ctr, updown);
+        int bits = 0;
+        while (bits < 40 && ((n - 1) >> bits) != 0) ++bits;            // bit length of n - 1
+        const int shift = bits > VAL_BINS_LB ? bits - VAL_BINS_LB : 0;
+        const i64 nch = num_chunks(m);
+        const unsigned grid = val_grid(m);
+        k_chunk_rows<<<nblk(nch, B), B, 0, st>>>(g->offsets, n, m, nch, v.CROW);
+        k_val_pass<false><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, shift, v.ctr, v.cnt,
+                                                       v.HIST, nullptr, nullptr);
         PG_LAUNCH_CHECK();
-        unsigned long long ud[2];
-        PG_CUDA_TRY(cudaMemcpyAsync(&h, w.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
-        PG_CUDA_TRY(cudaMemcpyAsync(ud, updown, sizeof ud, cudaMemcpyDeviceToHost, st));
+        unsigned long long c[3];
+        PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+        PG_CUDA_TRY(cudaMemcpyAsync(c, v.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaStreamSynchronize(st));
-        if (!(h.verr & (VERR_RANGE | VERR_UNSORTED)) && ud[0] != ud[1]) h.verr |= VERR_NOTSYM;
+        if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
+        if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
+        if (c[0] != c[1]) return PASGAL_ENOTSYM;
+        const i64 nkeys = (i64)c[2];
+        if (nkeys > 0) {
+            const i64 nh = (i64)VAL_BINS * grid;
+            PG_CUDA_TRY(launch_scan<u32>(nh, v.SCAN, 0u, SumOp(), ValHistLoad{v.HIST}, ValBaseStore{v.BASE},
+                                         (u32*)nullptr, st));
+            k_val_pass<true><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, shift, v.ctr, v.cnt,
+                                                          nullptr, v.BASE, v.KEYS);
+            k_val_check<<<nblk(nkeys, B), B, 0, st>>>(g->offsets, g->targets, v.KEYS, nkeys, v.ctr);
+            PG_LAUNCH_CHECK();
+            PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+            PG_CUDA_TRY(cudaStreamSynchronize(st));
+        }
     }
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;

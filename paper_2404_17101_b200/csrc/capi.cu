@@ -6,6 +6,8 @@ namespace pg {
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
                cudaStream_t st, pasgal_bcc_prof_t* prof);
 size_t bcc_workspace_bytes(i64 n, i64 m);
+size_t validate_workspace_bytes(i64 n, i64 m);
+int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st);
 size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
 int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
                         cudaStream_t st);
@@ -88,6 +90,12 @@ int pasgal_canonicalize(const pasgal_csr_t* g, const uint32_t* labels_in, int64_
     return pg::canonicalize_launch(g, labels_in, label_bound, labels_out, temp, temp_bytes, (cudaStream_t)stream);
 }
 
+size_t pasgal_csr_validate_workspace_bytes(int64_t n, int64_t m_slots) {
+    if (n < 0) n = 0;
+    if (m_slots < 0) m_slots = 0;
+    return pg::validate_workspace_bytes(n, m_slots);
+}
+
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {
     int s = check_csr(g);
     if (s) return s;
@@ -126,6 +134,11 @@ int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t*
                         void* temp, size_t temp_bytes, void* stream) {
     if ((npts > 0 && !keys) || !nkeys_dev || !temp) return PASGAL_EINVAL;
     return pg::gen_knn_keys(npts, k, seed, gbits, keys, nkeys_dev, temp, temp_bytes, (cudaStream_t)stream);
+}
+
+int pasgal_bits_to_bytes(const uint32_t* bits, int64_t n, uint8_t* bytes, void* stream) {
+    if (n < 0 || (n > 0 && (!bits || !bytes))) return PASGAL_EINVAL;
+    return pg::bits_to_bytes(bits, n, bytes, (cudaStream_t)stream);
 }
 
 const char* pasgal_strerror(int status) {

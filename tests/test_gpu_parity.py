@@ -268,3 +268,37 @@ def test_device_canonicaliser_and_comparator():
     off, tgt = _dev(path)
     lab = torch.from_numpy(path.label.astype(np.int32)).cuda()
     assert not pg.same_partition_device(off, tgt, lab, torch.zeros_like(lab))
+
+
+
+@pytest.mark.gpu
+def test_validator_random_perturbations_match_oracle():
+    """Device symmetry check == the oracle's is_symmetric (graph.py:123-158) on skewed
+    multigraphs with self-loops, symmetric or broken by one slot; the skew makes both
+    checker orientations (search the shorter row) occur."""
+    from tests import multigraph
+
+    rng = np.random.default_rng(2024)
+    kinds = {"sym": 0, "asym": 0}
+    for trial in range(300):
+        n, off, tgt = multigraph.perturbed(rng, trial)
+        want = oracle.is_symmetric(off, tgt)
+        kinds["sym" if want else "asym"] += 1
+        o = torch.from_numpy(off).cuda()
+        t = torch.from_numpy(tgt.view(np.int32)).cuda()
+        if want:
+            pg.validate_device(o, t)
+        else:
+            with pytest.raises(ValueError, match="symmetric"):
+                pg.validate_device(o, t)
+    assert kinds["sym"] > 50 and kinds["asym"] > 50
+
+
+def test_articulation_bytes_device_matches_host_unpack():
+    rng = np.random.default_rng(11)
+    for n in [1, 31, 32, 33, 1000, 4096 + 7]:
+        bits = rng.integers(0, 2 ** 32, (n + 31) // 32, dtype=np.uint64).astype(np.uint32)
+        d = torch.from_numpy(bits.view(np.int32)).cuda()
+        got = pg.articulation_bytes_device(d, n).cpu().numpy()
+        assert got.dtype == np.uint8 and got.shape == (n,)
+        assert np.array_equal(got.view(np.bool_), pg.unpack_articulation(bits, n))

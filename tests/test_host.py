@@ -96,6 +96,19 @@ def test_workspace_is_linear_in_n(lib):
         assert extra <= 4 * (m // 256 + 2) + 8 * (m // 2048 + 2) + 4096
 
 
+def test_validate_workspace_is_linear_in_m(lib):
+    """Validation scratch: one 8-byte key per run of up slots (<= m/2) plus per-CTA
+    histograms; an undersized workspace is refused before any device work."""
+    for n, m in [(1, 0), (1000, 10), (1 << 20, 50 << 20), (1 << 28, 16 << 28)]:
+        need = lib.pasgal_csr_validate_workspace_bytes(n, m)
+        assert 4 * m <= need <= 4 * m + m // 64 + 2 * 4096 * 1184 + (1 << 20)
+    from paper_2404_17101_b200 import _lib
+
+    csr = _lib.PasgalCsr(10, 20, 0x1000, 0x2000)
+    need = lib.pasgal_csr_validate_workspace_bytes(10, 20)
+    assert lib.pasgal_csr_validate(ctypes.byref(csr), ctypes.c_void_p(0x3000), need - 1, None) == _lib.PASGAL_EWORKSPACE
+
+
 def test_results_mirror_matches_reference_comparator():
     from paper_2404_17101_b200.results import BccLabels, canonical_edge_partition, canonical_relabel
 

@@ -186,3 +186,40 @@ def test_tags_write_protocol():
             want = [int(first[r]), int(first[r])] if seg.shape[0] == 0 else \
                 [min(int(first[r]), int(seg.min())), max(int(first[r]), int(seg.max()))]
             assert W[r] == want, (trial, r)
+
+
+def _validator_rule(off, tgt):
+    """Slot-level restatement of k_validate_slots: checker iff (deg w, w) < (deg u, u);
+    a checker finds its own copy of u in row w; checker and non-checker counts balance."""
+    import bisect
+
+    n = off.shape[0] - 1
+    up = down = 0
+    for u in range(n):
+        for s in range(off[u], off[u + 1]):
+            w = int(tgt[s])
+            if w == u:
+                continue
+            du, dw = off[u + 1] - off[u], off[w + 1] - off[w]
+            if not (dw < du or (dw == du and w < u)):
+                down += 1
+                continue
+            up += 1
+            k = 0
+            while s - k - 1 >= off[u] and tgt[s - k - 1] == w:
+                k += 1
+            row = tgt[off[w]:off[w + 1]].tolist()
+            q = bisect.bisect_left(row, u) + k
+            if q >= len(row) or row[q] != u:
+                return False
+    return up == down
+
+
+def test_validator_checker_rule_equals_oracle_is_symmetric():
+    import oracle
+    from tests import multigraph
+
+    rng = np.random.default_rng(7)
+    for trial in range(600):
+        _, off, tgt = multigraph.perturbed(rng, trial)
+        assert _validator_rule(off, tgt) == oracle.is_symmetric(off, tgt), trial
