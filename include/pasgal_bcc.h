@@ -187,6 +187,41 @@ int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t*
                         int64_t* nkeys_dev, void* temp, size_t temp_bytes, void* stream);
 
 /* Human-readable status text. */
+/* Text adjacency graph files (load_adj, graph.py:250-318) parsed on the
+ * device.  The caller puts the raw file bytes in device memory and calls, in order:
+ *   pasgal_adj_tokenize        -> number of whitespace-separated tokens (synchronises);
+ *   pasgal_adj_token_position  -> {byte, 1-based line} of token k ({nbytes, last line} if
+ *                                 k >= ntokens), for header / count tokens and messages;
+ *   pasgal_adj_parse           -> offsets int64[n+1] (offsets[n] = m) and targets int32[m]
+ *                                 from tokens 3.., given n and m from the header tokens,
+ *                                 plus first_err[PASGAL_ADJ_NERR]: per error class the
+ *                                 first offending element index (-1: none).  Weights
+ *                                 (WeightedAdjacencyGraph) are checked, not stored; a
+ *                                 negative weight with a tiny exponent may round to -0.0
+ *                                 and is listed in `uncertain` (up to PASGAL_ADJ_UNC_CAP;
+ *                                 *n_uncertain is the full count) for the caller to decide.
+ * The same temp buffer (pasgal_adj_temp_bytes(nbytes)) must be passed to all three. */
+enum {
+    PASGAL_ADJ_INV_OFFSET = 0,   /* offset token not an int64 literal */
+    PASGAL_ADJ_OVF_OFFSET = 1,   /* offset literal outside int64 */
+    PASGAL_ADJ_RANGE_OFFSET = 2, /* offset < 0 or > m */
+    PASGAL_ADJ_INV_TARGET = 3,
+    PASGAL_ADJ_OVF_TARGET = 4,
+    PASGAL_ADJ_RANGE_TARGET = 5, /* target < 0 or >= n */
+    PASGAL_ADJ_INV_WEIGHT = 6,   /* weight token not a float literal */
+    PASGAL_ADJ_BAD_WEIGHT = 7,   /* weight fails w >= 0 (negative, -inf, nan) */
+    PASGAL_ADJ_NERR = 8
+};
+#define PASGAL_ADJ_UNC_CAP 1024
+size_t pasgal_adj_temp_bytes(int64_t nbytes);
+int pasgal_adj_tokenize(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t* ntokens,
+                        void* stream);
+int pasgal_adj_token_position(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t k,
+                              int64_t* byte_line, void* stream);
+int pasgal_adj_parse(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t n, int64_t m,
+                     int weighted, int64_t* offsets, int32_t* targets, int64_t* first_err, int64_t* uncertain,
+                     int64_t* n_uncertain, void* stream);
+
 /* Articulation bitmap -> one byte per vertex (0/1), on the device: the reference's
  * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.
  * Asynchronous on `stream`. */

@@ -8,6 +8,12 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, siz
 size_t bcc_workspace_bytes(i64 n, i64 m);
 size_t validate_workspace_bytes(i64 n, i64 m);
 int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st);
+size_t adj_temp_bytes(i64 L);
+int adj_tokenize(const uint8_t* text, i64 L, void* temp, size_t temp_bytes, int64_t* ntokens, cudaStream_t st);
+int adj_token_position(const uint8_t* text, i64 L, void* temp, size_t temp_bytes, i64 k, int64_t* byte_line,
+                       cudaStream_t st);
+int adj_parse(const uint8_t* text, i64 L, void* temp, size_t temp_bytes, i64 n, i64 m, int weighted, i64* offsets,
+              int32_t* targets, int64_t* first_err, int64_t* uncertain, int64_t* n_uncertain, cudaStream_t st);
 size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
 int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
                         cudaStream_t st);
@@ -134,6 +140,33 @@ int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t*
                         void* temp, size_t temp_bytes, void* stream) {
     if ((npts > 0 && !keys) || !nkeys_dev || !temp) return PASGAL_EINVAL;
     return pg::gen_knn_keys(npts, k, seed, gbits, keys, nkeys_dev, temp, temp_bytes, (cudaStream_t)stream);
+}
+
+size_t pasgal_adj_temp_bytes(int64_t nbytes) { return pg::adj_temp_bytes(nbytes < 0 ? 0 : nbytes); }
+
+int pasgal_adj_tokenize(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t* ntokens,
+                        void* stream) {
+    if (nbytes < 0 || (nbytes > 0 && !text) || !ntokens) return PASGAL_EINVAL;
+    if (!temp) return PASGAL_EWORKSPACE;
+    return pg::adj_tokenize(text, nbytes, temp, temp_bytes, ntokens, (cudaStream_t)stream);
+}
+
+int pasgal_adj_token_position(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t k,
+                              int64_t* byte_line, void* stream) {
+    if (nbytes < 0 || (nbytes > 0 && !text) || k < 0 || !byte_line) return PASGAL_EINVAL;
+    if (!temp) return PASGAL_EWORKSPACE;
+    return pg::adj_token_position(text, nbytes, temp, temp_bytes, k, byte_line, (cudaStream_t)stream);
+}
+
+int pasgal_adj_parse(const uint8_t* text, int64_t nbytes, void* temp, size_t temp_bytes, int64_t n, int64_t m,
+                     int weighted, int64_t* offsets, int32_t* targets, int64_t* first_err, int64_t* uncertain,
+                     int64_t* n_uncertain, void* stream) {
+    if (nbytes < 0 || (nbytes > 0 && !text) || n < 0 || n >= ((int64_t)1 << 31) || m < 0 ||
+        m >= ((int64_t)1 << 32) || !offsets || (m > 0 && !targets) || !first_err)
+        return PASGAL_EINVAL;
+    if (!temp) return PASGAL_EWORKSPACE;
+    return pg::adj_parse(text, nbytes, temp, temp_bytes, n, m, weighted, offsets, targets, first_err, uncertain,
+                         n_uncertain, (cudaStream_t)stream);
 }
 
 int pasgal_bits_to_bytes(const uint32_t* bits, int64_t n, uint8_t* bytes, void* stream) {
