@@ -222,6 +222,23 @@ int pasgal_adj_parse(const uint8_t* text, int64_t nbytes, void* temp, size_t tem
                      int weighted, int64_t* offsets, int32_t* targets, int64_t* first_err, int64_t* uncertain,
                      int64_t* n_uncertain, void* stream);
 
+/* Bit-parallel BFS from up to 64 sources at once: the searches of
+ * estimate_diameter (graph.py:557-605) and the exact hop distances of bfs_queue
+ * (oracles.py:27-46).  Works on any CSR (directed or symmetric); `sources` is a HOST array
+ * of nsources in [1, 64] ids in [0, n).  ecc[i] (host) = eccentricity of sources[i] (the
+ * largest hop distance it reaches); *levels (host) = the number of BFS levels.  With
+ * nsources == 1, `dist` (device int32[n], nullable) receives hop distances, -1 where
+ * unreachable.  SYNCHRONISES `stream`.  Workspace: pasgal_msbfs_workspace_bytes(n). */
+size_t pasgal_msbfs_workspace_bytes(int64_t n);
+int pasgal_msbfs(const pasgal_csr_t* g, const int64_t* sources, int nsources, int32_t* dist, int64_t* ecc,
+                 int64_t* levels, void* workspace, size_t workspace_bytes, void* stream);
+/* pasgal_msbfs plus probes: probe (device int32[n]) maps a vertex to a probe index in
+ * [0, nprobe) or -1; probe_dist (device int32[nsources * nprobe]) receives the hop distance
+ * from source i to probe j at [i * nprobe + j], -1 if unreachable. */
+int pasgal_msbfs_ex(const pasgal_csr_t* g, const int64_t* sources, int nsources, int32_t* dist, int64_t* ecc,
+                    int64_t* levels, const int32_t* probe, int64_t nprobe, int32_t* probe_dist, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* Articulation bitmap -> one byte per vertex (0/1), on the device: the reference's
  * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.
  * Asynchronous on `stream`. */

@@ -15,6 +15,8 @@ This package is the checker, never the product.  Only ``tests/``,
 * ``canonical_min_eid`` -- the parity comparator: every slot labelled by the minimum
   undirected edge id of its BCC (order-isomorphic to
   ``results.canonical_edge_partition``, results.py:103-112).
+* ``bfs_queue`` / ``estimate_diameter`` -- C restatement of the reference's FIFO BFS
+  (oracles.py:27-46, graph.py:557-605), pinned by tests/golden/bfs_cases.npz.
 * ``gen_grid`` / ``rmat`` / ``knn`` -- host twins of the device generators
   (rules pinned in DESIGN.md, "Generators").
 """
@@ -56,6 +58,8 @@ def _load():
     lib.oracle_canonical_min_eid.restype = ctypes.c_int
     lib.oracle_connected_components.argtypes = [ctypes.c_int64, _i64p, _u32p, _i32p]
     lib.oracle_connected_components.restype = ctypes.c_int64
+    lib.oracle_bfs.argtypes = [ctypes.c_int64, _i64p, _u32p, ctypes.c_int64, _i32p]
+    lib.oracle_bfs.restype = ctypes.c_int64
     lib.oracle_count_upper.argtypes = [ctypes.c_int64, _i64p, _u32p]
     lib.oracle_count_upper.restype = ctypes.c_int64
     lib.host_csr_from_keys.argtypes = [ctypes.c_int64, _u64p, ctypes.c_int64, _i64p, _u32p]
@@ -155,6 +159,34 @@ def connected_components(offsets, targets):
     if c < 0:
         raise MemoryError("oracle allocation failed")
     return comp[:n], int(c)
+
+
+def bfs_queue(offsets, targets, source):
+    """oracles.bfs_queue (oracles.py:27-46) in C: (dist int64[n] with -1 = unreachable,
+    eccentricity of the source)."""
+    lib = _load()
+    off, tgt = _csr(offsets, targets)
+    n = off.shape[0] - 1
+    if not 0 <= source < n:
+        raise ValueError(f"source {source} out of range for n={n}")
+    dist = np.empty(max(n, 1), dtype=np.int32)
+    ecc = lib.oracle_bfs(n, _p(off, _i64p), _p(tgt, _u32p), int(source), _p(dist, _i32p))
+    if ecc < 0:
+        raise MemoryError("oracle allocation failed")
+    return dist[:n].astype(np.int64), int(ecc)
+
+
+def estimate_diameter(offsets, targets, samples=1000, seed=0):
+    """graph.estimate_diameter (graph.py:595-605): max eccentricity over the reference's
+    default_rng(seed) source sample, one C BFS per source."""
+    off, tgt = _csr(offsets, targets)
+    n, m = off.shape[0] - 1, tgt.shape[0]
+    if samples < 1:
+        raise ValueError("samples must be >= 1")
+    if n == 0 or m == 0:
+        return 0
+    sources = np.random.default_rng(seed).integers(0, n, size=samples, dtype=np.int64)
+    return max(bfs_queue(off, tgt, int(s))[1] for s in sources)
 
 
 def count_upper(offsets, targets):

@@ -258,3 +258,32 @@ int64_t oracle_connected_components(int64_t n, const int64_t* off, const uint32_
     free(queue);
     return count;
 }
+
+/* ------------------------------------------------------------------------- */
+/* FIFO BFS (oracles.bfs_queue, oracles.py:27-46; graph._bfs_ecc, graph.py:557-576):  */
+/* dist[v] = hop distance from source, -1 where unreachable; returns the         */
+/* eccentricity (largest distance reached), or a negative error.                 */
+/* ------------------------------------------------------------------------- */
+int64_t oracle_bfs(int64_t n, const int64_t* off, const uint32_t* tgt, int64_t source, int32_t* dist) {
+    if (source < 0 || source >= n) return -ORC_NOT_SYMMETRIC - 100;
+    int32_t* queue = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    if (!queue) return -ORC_NOMEM;
+    for (int64_t v = 0; v < n; ++v) dist[v] = -1;
+    int64_t head = 0, tail = 0, ecc = 0;
+    dist[source] = 0;
+    queue[tail++] = (int32_t)source;
+    while (head < tail) {
+        int64_t u = queue[head++];
+        int32_t du = dist[u];
+        if (du > ecc) ecc = du;
+        for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+            int64_t w = tgt[e];
+            if (dist[w] == -1) {
+                dist[w] = du + 1;
+                queue[tail++] = (int32_t)w;
+            }
+        }
+    }
+    free(queue);
+    return ecc;
+}

@@ -9,6 +9,9 @@ size_t bcc_workspace_bytes(i64 n, i64 m);
 size_t validate_workspace_bytes(i64 n, i64 m);
 int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st);
 size_t adj_temp_bytes(i64 L);
+size_t msbfs_workspace_bytes(i64 n, i64 max_levels);
+int msbfs(const pasgal_csr_t* g, const int64_t* sources, int ns, int32_t* dist, int64_t* ecc, int64_t* levels,
+          const int32_t* probe, i64 nprobe, int32_t* probe_dist, void* ws, size_t ws_bytes, cudaStream_t st);
 int adj_tokenize(const uint8_t* text, i64 L, void* temp, size_t temp_bytes, int64_t* ntokens, cudaStream_t st);
 int adj_token_position(const uint8_t* text, i64 L, void* temp, size_t temp_bytes, i64 k, int64_t* byte_line,
                        cudaStream_t st);
@@ -140,6 +143,32 @@ int pasgal_gen_knn_keys(int64_t npts, int k, uint64_t seed, int gbits, uint64_t*
                         void* temp, size_t temp_bytes, void* stream) {
     if ((npts > 0 && !keys) || !nkeys_dev || !temp) return PASGAL_EINVAL;
     return pg::gen_knn_keys(npts, k, seed, gbits, keys, nkeys_dev, temp, temp_bytes, (cudaStream_t)stream);
+}
+
+size_t pasgal_msbfs_workspace_bytes(int64_t n) {
+    if (n < 0) n = 0;
+    return pg::msbfs_workspace_bytes(n, n);
+}
+
+int pasgal_msbfs(const pasgal_csr_t* g, const int64_t* sources, int nsources, int32_t* dist, int64_t* ecc,
+                 int64_t* levels, void* workspace, size_t workspace_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!sources || !ecc || nsources < 1 || nsources > 64) return PASGAL_EINVAL;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::msbfs(g, sources, nsources, dist, ecc, levels, nullptr, 0, nullptr, workspace, workspace_bytes,
+                     (cudaStream_t)stream);
+}
+
+int pasgal_msbfs_ex(const pasgal_csr_t* g, const int64_t* sources, int nsources, int32_t* dist, int64_t* ecc,
+                    int64_t* levels, const int32_t* probe, int64_t nprobe, int32_t* probe_dist, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!sources || !ecc || nsources < 1 || nsources > 64 || nprobe < 0) return PASGAL_EINVAL;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::msbfs(g, sources, nsources, dist, ecc, levels, probe, nprobe, probe_dist, workspace, workspace_bytes,
+                     (cudaStream_t)stream);
 }
 
 size_t pasgal_adj_temp_bytes(int64_t nbytes) { return pg::adj_temp_bytes(nbytes < 0 ? 0 : nbytes); }
