@@ -118,6 +118,16 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
 int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* pasgal_csr_validate in two halves, so the symmetry check can be scheduled around
+ * FAST-BCC.  _begin runs and WAITS FOR the streaming checks (ranges, row order, equal
+ * numbers of up and down slots) -- once it returns PASGAL_OK the CSR is safe to pass to
+ * pasgal_bcc; a nonzero status is final.  _end launches the bucketed symmetry check on
+ * `stream`, waits for it and returns the final status; ordering `stream` after the BCC
+ * kernels (an event) lets it run while the labels are copied to the host.  Same workspace
+ * for both, untouched in between. */
+int pasgal_csr_validate_begin(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream);
+int pasgal_csr_validate_end(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Workspace for pasgal_csr_validate: 4 bytes per slot (one bucketed 8-byte key per run of
  * "up" slots, at most m/2 of them) plus ~8 KB per CTA of histograms -- O(m), like the
  * reference's twin array (oracles.py:107-116).  May alias pasgal_bcc's workspace. */

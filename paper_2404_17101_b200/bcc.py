@@ -35,19 +35,65 @@ def validate_workspace_bytes(n, m):
     return int(_lib.load().pasgal_csr_validate_workspace_bytes(int(n), int(m)))
 
 
-def _workspace(device, nbytes):
-    """A cached device workspace of at least nbytes (the library never allocates)."""
-    key = torch.device(device)
+def _workspace(device, nbytes, kind="bcc"):
+    """A cached device workspace of at least nbytes (the library never allocates).
+    ``kind`` separates buffers that are in use at the same time (BCC and validation)."""
+    key = (kind, torch.device(device))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
         _ws_cache.pop(key, None)
-        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=key)
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=key[1])
         _ws_cache[key] = ws
     return ws
 
 
 def release_workspace():
     _ws_cache.clear()
+    _side_streams.clear()
+    _priority_streams.clear()
+
+
+_side_streams = {}
+
+
+def _side_stream(device):
+    dev = torch.device(device)
+    if dev not in _side_streams:
+        _side_streams[dev] = torch.cuda.Stream(dev, priority=0)    # 0 = the lowest priority
+    return _side_streams[dev]
+
+
+class _PendingValidation:
+    """Second half of a split validation (pasgal_csr_validate_end): the symmetry check,
+    run on the side stream after `after` (an event: the BCC kernels) so it overlaps
+    whatever follows them on the main stream (the labels' D2H copy)."""
+
+    def __init__(self, csr, ws, stream, keep):
+        self.csr, self.ws, self.stream, self.keep = csr, ws, stream, keep
+
+    def finish(self, after=None):
+        if after is not None:
+            self.stream.wait_event(after)
+        st = _lib.load().pasgal_csr_validate_end(ctypes.byref(self.csr), _vp(self.ws), self.ws.numel(),
+                                                 ctypes.c_void_p(self.stream.cuda_stream))
+        self.keep = None
+        _lib.check(st, "validate")
+
+
+def _validate_begin(offsets, targets):
+    """Run the blocking streaming checks now (ranges, row order, up/down balance: after
+    this the CSR is safe for FAST-BCC); the symmetry check is the returned object's
+    finish().  Raises at once on an early failure."""
+    lib = _lib.load()
+    dev = offsets.device
+    n, m = offsets.shape[0] - 1, targets.shape[0]
+    ws = _workspace(dev, validate_workspace_bytes(n, m), kind="validate")
+    side = _side_stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))        # the CSR's H2D copies
+    csr = _csr_struct(offsets, targets)
+    st = lib.pasgal_csr_validate_begin(ctypes.byref(csr), _vp(ws), ws.numel(), ctypes.c_void_p(side.cuda_stream))
+    _lib.check(st, "validate")
+    return _PendingValidation(csr, ws, side, (offsets, targets))
 
 
 @dataclass
@@ -77,7 +123,8 @@ def validate_device(offsets, targets, workspace=None):
     lib = _lib.load()
     n, m = offsets.shape[0] - 1, targets.shape[0]
     need = validate_workspace_bytes(n, m)
-    ws = workspace if workspace is not None and workspace.numel() >= need else _workspace(offsets.device, need)
+    ws = (workspace if workspace is not None and workspace.numel() >= need
+          else _workspace(offsets.device, need, kind="validate"))
     csr = _csr_struct(offsets, targets)
     st = lib.pasgal_csr_validate(ctypes.byref(csr), _vp(ws), ws.numel(),
                                  ctypes.c_void_p(torch.cuda.current_stream(offsets.device).cuda_stream))
@@ -85,7 +132,7 @@ def validate_device(offsets, targets, workspace=None):
 
 
 def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out=None,
-               workspace=None, forest=False, events=None):
+               workspace=None, forest=False, events=None, _defer_validation=False):
     """FAST-BCC on a device CSR (offsets int64[n+1], targets int32[M], both CUDA).
 
     Returns ``DeviceBcc``.  ``canonical=True`` labels every edge with the minimum
@@ -103,13 +150,12 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
     n, m = offsets.shape[0] - 1, targets.shape[0]
     dev = offsets.device
     need = workspace_bytes(n, m)
-    if validate and workspace is None:
-        need = max(need, validate_workspace_bytes(n, m))   # one cached buffer serves both
     ws = workspace if workspace is not None else _workspace(dev, need)
     if ws.numel() < need:
         raise ValueError("workspace too small")
-    if validate:
-        validate_device(offsets, targets, ws)
+    # validation is split: its streaming half gates the call, its symmetry half runs after
+    # the BCC kernels on a side stream (overlapping the caller's next copies when deferred)
+    pending = _validate_begin(offsets, targets) if validate else None
     if out is None:
         out = DeviceBcc(
             edge_label=torch.empty(m, dtype=torch.int32, device=dev),
@@ -139,8 +185,14 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
         prof = _lib.PasgalBccProf(ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), len(handles), 0)
     st = lib.pasgal_bcc_ex(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
                            flags, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prof))
+    if st != 0 and pending is not None:
+        pending.finish()            # a symmetry error explains a failure better
     _lib.check(st, "bcc")
     out.launches = prof.launches
+    if pending is not None:
+        if _defer_validation:
+            return out, pending
+        pending.finish()
     return out
 
 
@@ -243,7 +295,34 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
     the device, validated there (``ValueError("biconnectivity requires a symmetric graph")``
     as in oracles.py:127-128), processed, and the labels, articulation flags and count are
     copied back into a ``BccLabels``.  Rows must be sorted (every reference builder sorts).
+
+    The work runs on a high-priority stream: the validation's symmetry check, on the
+    lowest-priority side stream, then only fills the SMs the BCC kernels leave idle
+    instead of delaying them (its ~8M-block grid would otherwise be dispatched first).
     """
+    dev = torch.device(device) if not isinstance(g, DeviceGraph) else g.offsets.device
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    cur = torch.cuda.current_stream(dev)
+    hp = _priority_stream(dev)
+    hp.wait_stream(cur)
+    with torch.cuda.stream(hp):
+        res = _bcc_host(g, seed, validate, canonical, device, forest, host_out)
+    cur.wait_stream(hp)
+    return res
+
+
+_priority_streams = {}
+
+
+def _priority_stream(device):
+    if device not in _priority_streams:
+        # torch maps an out-of-range priority to the nearest valid one: the greatest here
+        _priority_streams[device] = torch.cuda.Stream(device, priority=-100)
+    return _priority_streams[device]
+
+
+def _bcc_host(g, seed, validate, canonical, device, forest, host_out):
     if isinstance(g, DeviceGraph):
         off_d, tgt_d = g.offsets, g.targets
     else:
@@ -263,15 +342,25 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
         tgt_d = torch.from_numpy(tgt).to(device, non_blocking=True)
     n = off_d.shape[0] - 1
     m = tgt_d.shape[0]
-    r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest)
+    r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest,
+                   _defer_validation=validate)
+    pending = None
+    if validate:
+        r, pending = r
     art_d = articulation_bytes_device(r.artic_bits, n)
+    done = torch.cuda.Event()
+    done.record()                           # BCC kernels + articulation bytes
     if host_out is not None:
         host_out.edge_label[:m].copy_(r.edge_label, non_blocking=True)
         host_out.articulation[:n].copy_(art_d, non_blocking=True)
+        if pending is not None:
+            pending.finish(after=done)      # the symmetry check runs during the D2H above
         count = int(r.bcc_count.item())     # synchronises the stream
         lab = host_out.edge_label[:m].numpy().view(np.uint32)
         art = host_out.articulation[:n].numpy().view(np.bool_)
     else:
+        if pending is not None:
+            pending.finish(after=done)
         lab = r.edge_label.cpu().numpy().view(np.uint32)
         art = art_d.cpu().numpy().view(np.bool_)
         count = int(r.bcc_count.item())

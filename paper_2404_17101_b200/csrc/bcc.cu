@@ -1593,7 +1593,23 @@ int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st) {
     return PASGAL_OK;
 }
 
-int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+static int val_status(u32 verr) {
+    if (verr & VERR_RANGE) return PASGAL_ERANGE;
+    if (verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
+    if (verr & VERR_NOTSYM) return PASGAL_ENOTSYM;
+    return PASGAL_OK;
+}
+
+static int val_shift(i64 n) {
+    int bits = 0;
+    while (bits < 40 && ((n - 1) >> bits) != 0) ++bits;   // bit length of n - 1
+    return bits > VAL_BINS_LB ? bits - VAL_BINS_LB : 0;
+}
+
+// Validation, first half: the streaming checks (ranges, row order, #up == #down, and the
+// bucket histogram of the keys), waited for.  After PASGAL_OK the CSR is safe for
+// FAST-BCC.  A nonzero return is final.
+int csr_validate_begin(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
     const i64 n = g->n, m = g->m_slots;
     ValWs v;
     size_t need = carve_val(v, nullptr, n, m);
@@ -1608,40 +1624,56 @@ int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStrea
     PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
     PG_CUDA_TRY(cudaStreamSynchronize(st));
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
+    if (m == 0 || n == 0) return PASGAL_OK;
+    const i64 nch = num_chunks(m);
+    const unsigned grid = val_grid(m);
+    k_chunk_rows<<<nblk(nch, B), B, 0, st>>>(g->offsets, n, m, nch, v.CROW);
+    k_val_pass<false><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, val_shift(n), v.ctr, v.cnt,
+                                                   v.HIST, nullptr, nullptr);
+    PG_LAUNCH_CHECK();
+    unsigned long long c[3];
+    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaMemcpyAsync(c, v.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h.verr) return val_status(h.verr);
+    if (c[0] != c[1]) return PASGAL_ENOTSYM;
+    return PASGAL_OK;
+}
+
+// Validation, second half: the bucketed symmetry check (scan, key scatter, check),
+// launched on `st` and waited for; the final status.  The caller may order it after other
+// work (FAST-BCC) with an event, so it runs while the labels are copied out.
+int csr_validate_end(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+    const i64 n = g->n, m = g->m_slots;
+    ValWs v;
+    if (ws_bytes < carve_val(v, nullptr, n, m)) return PASGAL_EWORKSPACE;
+    carve_val(v, (char*)ws_ptr, n, m);
     if (m > 0 && n > 0) {
-        int bits = 0;
-        while (bits < 40 && ((n - 1) >> bits) != 0) ++bits;            // bit length of n - 1
-        const int shift = bits > VAL_BINS_LB ? bits - VAL_BINS_LB : 0;
-        const i64 nch = num_chunks(m);
-        const unsigned grid = val_grid(m);
-        k_chunk_rows<<<nblk(nch, B), B, 0, st>>>(g->offsets, n, m, nch, v.CROW);
-        k_val_pass<false><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, shift, v.ctr, v.cnt,
-                                                       v.HIST, nullptr, nullptr);
-        PG_LAUNCH_CHECK();
         unsigned long long c[3];
-        PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaMemcpyAsync(c, v.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaStreamSynchronize(st));
-        if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
-        if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
-        if (c[0] != c[1]) return PASGAL_ENOTSYM;
         const i64 nkeys = (i64)c[2];
-        if (nkeys > 0) {
+        const unsigned grid = val_grid(m);
+        const int B = 256;
+        if (nkeys > 0 && c[0] == c[1]) {
             const i64 nh = (i64)VAL_BINS * grid;
             PG_CUDA_TRY(launch_scan<u32>(nh, v.SCAN, 0u, SumOp(), ValHistLoad{v.HIST}, ValBaseStore{v.BASE},
                                          (u32*)nullptr, st));
-            k_val_pass<true><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, shift, v.ctr, v.cnt,
-                                                          nullptr, v.BASE, v.KEYS);
+            k_val_pass<true><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, val_shift(n), v.ctr,
+                                                          v.cnt, nullptr, v.BASE, v.KEYS);
             k_val_check<<<nblk(nkeys, B), B, 0, st>>>(g->offsets, g->targets, v.KEYS, nkeys, v.ctr);
             PG_LAUNCH_CHECK();
-            PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
-            PG_CUDA_TRY(cudaStreamSynchronize(st));
         }
     }
-    if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
-    if (h.verr & VERR_UNSORTED) return PASGAL_EUNSORTED;
-    if (h.verr & VERR_NOTSYM) return PASGAL_ENOTSYM;
-    return PASGAL_OK;
+    Ctr h;
+    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    PG_CUDA_TRY(cudaStreamSynchronize(st));
+    return val_status(h.verr);
+}
+
+int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+    int s = csr_validate_begin(g, ws_ptr, ws_bytes, st);
+    return s ? s : csr_validate_end(g, ws_ptr, ws_bytes, st);
 }
 
 }  // namespace pg

@@ -24,6 +24,8 @@ int csr_first_error(const pasgal_csr_t* g, void* scratch, int64_t* host_out, cud
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
               cudaStream_t st);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
+int csr_validate_begin(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
+int csr_validate_end(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gen_grid_temp_bytes(i64 rows, i64 cols);
 int gen_grid(i64 rows, i64 cols, u64 seed, u64 thr, int keep_all, i64* off, int32_t* tgt, i64* m_dev, void* temp,
              size_t temp_bytes, cudaStream_t st);
@@ -97,6 +99,20 @@ int pasgal_canonicalize(const pasgal_csr_t* g, const uint32_t* labels_in, int64_
         return PASGAL_EINVAL;
     if (!temp) return PASGAL_EWORKSPACE;
     return pg::canonicalize_launch(g, labels_in, label_bound, labels_out, temp, temp_bytes, (cudaStream_t)stream);
+}
+
+int pasgal_csr_validate_begin(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::csr_validate_begin(g, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int pasgal_csr_validate_end(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    return pg::csr_validate_end(g, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t pasgal_csr_validate_workspace_bytes(int64_t n, int64_t m_slots) {
