@@ -942,21 +942,47 @@ __global__ void k_compress_final(i64 n, u32* C, Ctr* ctr) {
 // a fence and whose skeleton component differs from its parent's heads a BCC hanging off
 // the parent; a non-root parent is then an articulation point, a root only if its head
 // children span >= 2 components.  P (First-CC) has P[x] == x exactly at tree roots.
+// Hubs: siblings with small subtrees sit at adjacent positions, so a warp first groups runs
+// of adjacent lanes with one parent (one update per run; two components within a run
+// already decide a root), and the bit and
+// the write-once ROOTMARK are read before any atomic -- a 33M-leaf star otherwise spent
+// 21 ms in same-address atomics on the hub.
 __global__ void k_artic(i64 n, const u32* __restrict__ PPAR, const u32* __restrict__ FPF, const u32* __restrict__ C,
                         const u32* __restrict__ P, u32* ROOTMARK, u32* bits) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    u32 f = FPF[i];
-    if (f == PG_INV || !(f & 0x80000000u)) return;
-    u32 ci = C[i];
-    if (ci == C[f & 0x7FFFFFFFu]) return;  // fence child inside p's own component: not a head
-    u32 p = PPAR[i];
-    if (P[p] != p) {
-        atomicOr(bits + (p >> 5), 1u << (p & 31));
-    } else {
-        u32 old = atomicCAS(ROOTMARK + p, PG_INV, ci);
-        if (old != PG_INV && old != ci) atomicOr(bits + (p >> 5), 1u << (p & 31));
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool head = false;
+    u32 p = PG_INV, ci = 0;
+    if (i < n) {
+        const u32 f = FPF[i];
+        if (f != PG_INV && (f & 0x80000000u)) {
+            ci = C[i];
+            if (ci != C[f & 0x7FFFFFFFu]) {      // fence child inside p's own component: not a head
+                head = true;
+                p = PPAR[i];
+            }
+        }
     }
+    const unsigned hm = __ballot_sync(0xFFFFFFFFu, head);
+    if (!hm) return;                                         // warp-uniform
+    // groups = runs of adjacent head lanes with one parent (star leaves are adjacent)
+    const u32 pp = __shfl_up_sync(0xFFFFFFFFu, p, 1), pc = __shfl_up_sync(0xFFFFFFFFu, ci, 1);
+    const bool cont = head && lane > 0 && (hm >> (lane - 1) & 1u) && pp == p;
+    const unsigned lead = hm & ~__ballot_sync(0xFFFFFFFFu, cont);        // first lane of each run
+    const unsigned mism = __ballot_sync(0xFFFFFFFFu, cont && pc != ci);   // run spans >= 2 components
+    if (!(lead >> lane & 1u)) return;
+    const unsigned after = lead & ~((2u << lane) - 1u);                  // later run leaders
+    const unsigned run = (after ? (1u << (__ffs(after) - 1)) : 0u) - (1u << lane);   // this run's lanes
+    const bool differ = (mism & (after ? run : ~((1u << lane) - 1u))) != 0;
+    const u32 bit = 1u << (p & 31);
+    if (*(volatile u32*)(bits + (p >> 5)) & bit) return;    // already an articulation point
+    if (P[p] != p || differ) {
+        atomicOr(bits + (p >> 5), bit);
+        return;
+    }
+    u32 cur = *(volatile u32*)(ROOTMARK + p);               // write-once: PG_INV -> first head's cid
+    if (cur == PG_INV) cur = atomicCAS(ROOTMARK + p, PG_INV, ci);
+    if (cur != PG_INV && cur != ci) atomicOr(bits + (p >> 5), bit);
 }
 
 // per vertex (coalesced): CIDV[v] = component of position first[v] (one random read of the

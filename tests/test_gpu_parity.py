@@ -302,3 +302,20 @@ def test_articulation_bytes_device_matches_host_unpack():
         got = pg.articulation_bytes_device(d, n).cpu().numpy()
         assert got.dtype == np.uint8 and got.shape == (n,)
         assert np.array_equal(got.view(np.bool_), pg.unpack_articulation(bits, n))
+
+
+@pytest.mark.gpu
+def test_hub_shapes_match_oracle():
+    """Stars (root hub and non-root hub), a cycle of stars and a hub joined to a path:
+    articulation on hubs with millions of tree children (k_artic's per-warp grouping)."""
+    n = 1 << 22
+    leaves = np.arange(1, n)
+    shapes = [
+        (n, np.zeros(n - 1, np.int64), leaves),                                   # star, hub = root
+        (n, np.concatenate([[n - 1], np.full(n - 2, 5)]), np.concatenate([[0], np.delete(np.arange(n - 1), 5)])),
+        (n, np.concatenate([np.arange(1024), np.repeat(np.arange(1024), (n - 1024) // 1024)]),
+         np.concatenate([(np.arange(1024) + 1) % 1024, np.arange(1024, 1024 + ((n - 1024) // 1024) * 1024)])),
+    ]
+    for nv, s, t in shapes:
+        dg = pg.symmetrize_edges(nv, s, t)
+        _parity_device_graph(dg)
