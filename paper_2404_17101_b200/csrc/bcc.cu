@@ -60,8 +60,10 @@ struct Ctr {
     u32 giant2;   // sampled largest skeleton component (Last-CC)
     u32 ncomp;    // skeleton components
     u32 verr;     // validation error bits
-    u32 nheavy;   // heavy rows queued by k_cc_rest
-    u32 nheavy2;  // heavy rows queued by k_cc2_rest
+    u32 nheavy;   // heavy rows queued by k_cc_rest (HEAVY front)
+    u32 nheavy2;  // heavy rows queued by k_cc2_rest (HEAVY front)
+    u32 nvheavy;  // very heavy rows queued by k_cc_rest (HEAVY back, from index n-1 down)
+    u32 nvheavy2; // very heavy rows queued by k_cc2_rest (HEAVY back)
     u32 gcid;     // component id (head preorder rank) of the sampled giant skeleton component
 };
 
@@ -287,8 +289,16 @@ __global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u6
 
 // Rows outside the sampled giant component: a thread per vertex skips giant rows with one
 // read; rows longer than HEAVY_ROW slots go to a list served by a block per row, so a
-// stray hub never serialises on one thread.
+// stray hub never serialises on one thread, and rows longer than VHEAVY_ROW to a second
+// list whose rows are split over every block (one block per 2M-slot row took 4 ms).
+// Repeats of the previous slot's target (parallel edges) are skipped in the long rows.
 constexpr int HEAVY_ROW = 64;
+constexpr i64 VHEAVY_ROW = 1 << 16;
+
+__device__ __forceinline__ void queue_heavy(i64 n, i64 len, u32 u, u32* heavy, u32* nh, u32* nvh) {
+    if (len > VHEAVY_ROW) heavy[n - 1 - atomicAdd(nvh, 1u)] = u;
+    else heavy[atomicAdd(nh, 1u)] = u;
+}
 
 __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
                           Ctr* ctr, u32* heavy) {
@@ -297,19 +307,32 @@ __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __r
     i64 a = off[u] + NSAMPLE, b = off[u + 1];
     if (a >= b || ldcg(P + u) == ctr->giant) return;
     if (b - a > HEAVY_ROW) {
-        heavy[atomicAdd(&ctr->nheavy, 1u)] = (u32)u;
+        queue_heavy(n, b - a, (u32)u, heavy, &ctr->nheavy, &ctr->nvheavy);
         return;
     }
     for (i64 s = a; s < b; ++s) uf_link_hook(P, (u32)u, (u32)tgt[s], HAB);
 }
 
-__global__ void k_cc_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
-                                const Ctr* ctr, const u32* __restrict__ heavy) {
-    const u32 nh = ctr->nheavy;
+__global__ void k_cc_rest_heavy(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
+                                uint2* HAB, const Ctr* ctr, const u32* __restrict__ heavy) {
+    const u32 nh = ctr->nheavy, nvh = ctr->nvheavy;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         u32 u = heavy[h];
         i64 a = off[u] + NSAMPLE, b = off[u + 1];
-        for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) uf_link_hook(P, u, (u32)tgt[s], HAB);
+        for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) {
+            const int32_t w = tgt[s];
+            if (s > off[u] && tgt[s - 1] == w) continue;
+            uf_link_hook(P, u, (u32)w, HAB);
+        }
+    }
+    for (u32 h = 0; h < nvh; ++h) {
+        u32 u = heavy[n - 1 - h];
+        i64 a = off[u] + NSAMPLE, b = off[u + 1];
+        for (i64 s = a + (i64)blockIdx.x * blockDim.x + threadIdx.x; s < b; s += (i64)gridDim.x * blockDim.x) {
+            const int32_t w = tgt[s];
+            if (s > off[u] && tgt[s - 1] == w) continue;
+            uf_link_hook(P, u, (u32)w, HAB);
+        }
     }
 }
 
@@ -901,7 +924,7 @@ __global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __
     i64 a = off[u], b = off[u + 1];
     if (b - a < 2) return;
     if (b - a > HEAVY_ROW) {
-        heavy[atomicAdd(&ctr->nheavy2, 1u)] = u;
+        queue_heavy(n, b - a, u, heavy, &ctr->nheavy2, &ctr->nvheavy2);
         return;
     }
     uint2 fu = make_uint2((u32)i, E[i]);
@@ -911,14 +934,27 @@ __global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __
     }
 }
 
-__global__ void k_cc2_rest_heavy(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
+__global__ void k_cc2_rest_heavy(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                  const uint2* __restrict__ FL, u32* C, const Ctr* ctr, const u32* __restrict__ heavy) {
-    const u32 nh = ctr->nheavy2;
+    const u32 nh = ctr->nheavy2, nvh = ctr->nvheavy2;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         u32 u = heavy[h];
         uint2 fu = FL[u];
         for (i64 s = off[u] + threadIdx.x; s < off[u + 1]; s += blockDim.x) {
-            uint2 fw = FL[(u32)tgt[s]];
+            const int32_t w = tgt[s];
+            if (s > off[u] && tgt[s - 1] == w) continue;
+            uint2 fw = FL[(u32)w];
+            if (is_cross(fu, fw)) uf_link(C, fu.x, fw.x);
+        }
+    }
+    for (u32 h = 0; h < nvh; ++h) {
+        u32 u = heavy[n - 1 - h];
+        uint2 fu = FL[u];
+        for (i64 s = off[u] + (i64)blockIdx.x * blockDim.x + threadIdx.x; s < off[u + 1];
+             s += (i64)gridDim.x * blockDim.x) {
+            const int32_t w = tgt[s];
+            if (s > off[u] && tgt[s - 1] == w) continue;
+            uint2 fw = FL[(u32)w];
             if (is_cross(fu, fw)) uf_link(C, fu.x, fw.x);
         }
     }
@@ -1379,7 +1415,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
-    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
+    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
     // no final compress: later stages only ask "is x a root", and P[x] == x exactly at roots
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
@@ -1424,7 +1460,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
-    PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
+    PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
     PG_K(k_compress_final<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C, w.ctr));
     PG_K(k_cid_vertices<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FIRST, w.ctr, w.CIDV, w.GBIT, out->comp));
     PG_LAUNCH_CHECK();
@@ -1492,7 +1528,7 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
         k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
         k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
-        k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
+        k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
         k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
     }

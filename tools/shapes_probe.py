@@ -33,7 +33,25 @@ def shapes(scale):
     # binary tree (deep-ish, wide)
     v = np.arange(1, n)
     out["binary_tree"] = (n, (v - 1) // 2, v)
+    out["matching"] = (n, np.arange(0, n, 2), np.arange(1, n, 2))
+    out["selfloops_path"] = (n, np.concatenate([np.arange(n), np.arange(n - 1)]),
+                             np.concatenate([np.arange(n), np.arange(1, n)]))
+    out["k2n"] = (n, np.concatenate([np.zeros(n - 2, np.int64), np.ones(n - 2, np.int64)]),
+                  np.concatenate([np.arange(2, n), np.arange(2, n)]))
     return out
+
+
+def multi(scale):
+    """one edge with multiplicity 2^(scale-3), plus a path (CSR built by hand: symmetrize
+    would deduplicate)."""
+    n = 1 << (scale - 3)
+    k = 1 << (scale - 3)
+    src = np.concatenate([np.zeros(k, np.int64), np.ones(k, np.int64), np.arange(1, n - 1), np.arange(2, n)])
+    dst = np.concatenate([np.ones(k, np.int64), np.zeros(k, np.int64), np.arange(2, n), np.arange(1, n - 1)])
+    order = np.lexsort((dst, src))
+    src, dst = src[order], dst[order]
+    off = np.concatenate([[0], np.cumsum(np.bincount(src, minlength=n))]).astype(np.int64)
+    return n, off, dst.astype(np.uint32)
 
 
 def main():
@@ -41,8 +59,13 @@ def main():
     ap.add_argument("--scale", type=int, default=25)
     ap.add_argument("--parity", action="store_true")
     a = ap.parse_args()
-    for name, (n, s, t) in shapes(a.scale).items():
-        dg = pg.symmetrize_edges(n, s, t)
+    items = [(k, pg.symmetrize_edges(v[0], v[1], v[2])) for k, v in shapes(a.scale).items()]
+    n_m, off_m, tgt_m = multi(a.scale)
+    items.append(("multiedge_path", pg.DeviceGraph(torch.from_numpy(off_m).cuda(),
+                                                   torch.from_numpy(tgt_m.view(np.int32)).cuda())))
+    for name, dg in items:
+        n = dg.n
+        pg.validate_device(dg.offsets, dg.targets)
         torch.cuda.synchronize()
         pg.bcc_device(dg.offsets, dg.targets)
         torch.cuda.synchronize()
