@@ -399,9 +399,9 @@ constexpr u64 M31 = (1ull << 31) - 1;
 
 struct IsoOut {
     uint2* FL;
-    u32 *FIRST, *PV, *E, *PPAR;
+    u32 *PV, *E, *PPAR;
     uint2* W;
-    u32 *out_parent, *out_first, *ROOTMARK;
+    u32* ROOTMARK;
 };
 
 // One block = AC_B threads x AC_V vertices.  Both the isolated-slot counter and the root
@@ -480,13 +480,10 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restri
         if (slot[i] == PG_INV) continue;
         const u32 v = (u32)(base + (i64)i * AC_B), f = s_base + slot[i];
         io.FL[v] = make_uint2(f, f);
-        io.FIRST[v] = f;
         io.PV[f] = v;
         io.E[f] = f;
         io.PPAR[f] = v;
         io.W[f] = make_uint2(f, f);
-        if (io.out_parent) io.out_parent[v] = v;
-        if (io.out_first) io.out_first[v] = f;
     }
 }
 
@@ -608,10 +605,8 @@ struct PreStore {
     const u32* TP;
     const Ctr* ctr;
     uint2* FL;
-    u32* FIRST;
     u32 *PV, *E, *PPAR;
     uint2* W;
-    u32 *out_parent, *out_first;
     __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
         if (!down) return;
         f += ctr->niso;                   // isolated vertices occupy [0, niso)
@@ -621,16 +616,26 @@ struct PreStore {
         u32 last = f + (pt - (u32)k + 1) / 2 - 1;
         u32 par = TP[k];                 // source of the down arc p->v
         (void)lo;
-        FL[v] = make_uint2(f, last);
-        FIRST[v] = f;
+        FL[v] = make_uint2(f, last);   // FIRST and the optional outputs: k_vertex_first
         PV[f] = v;
         E[f] = last;
         PPAR[f] = par;
         W[f] = make_uint2(f, f);
-        if (out_parent) out_parent[v] = par;
-        if (out_first) out_first[v] = f;
     }
 };
+
+// FIRST[v] = FL[v].x and the optional parent/first outputs, per vertex and coalesced: the
+// preorder store writes only FL by vertex (a random 8-byte write; a second random 4-byte
+// FIRST write cost a partial-sector read-modify-write per vertex)
+__global__ void k_vertex_first(i64 n, const uint2* __restrict__ FL, const u32* __restrict__ PPAR, u32* FIRST,
+                               u32* out_parent, u32* out_first) {
+    const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const u32 f = FL[v].x;
+    FIRST[v] = f;
+    if (out_first) out_first[v] = f;
+    if (out_parent) out_parent[v] = __ldg(PPAR + f);
+}
 
 // --------------------------------------------------------------------------
 // S4: tags  w1/w2[first[v]] = min/max(first[v], first[u] for all neighbours u)
@@ -1423,7 +1428,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
     PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
         n, w.HAB, w.HEAD, w.P, w.ctr, w.NEXT,
-        IsoOut{w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first, w.ROOTMARK}));
+        IsoOut{w.FL, w.PV, w.E, w.PPAR, w.W, w.ROOTMARK}));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
@@ -1439,9 +1444,11 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.HAB, w.T, w.TP, w.ctr, n},
-                                 PreStore{w.T, w.TP, w.ctr, w.FL, w.FIRST, w.PV, w.E, w.PPAR, w.W, out->parent, out->first},
+                                 PreStore{w.T, w.TP, w.ctr, w.FL, w.PV, w.E, w.PPAR, w.W},
                                  (u32*)nullptr, st));
     ++nl;
+    PG_K(k_vertex_first<<<nblk(n, B), B, 0, st>>>(n, w.FL, w.PPAR, w.FIRST, out->parent, out->first));
+    PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
     if (w.nch > 0) PG_K(k_tags<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
