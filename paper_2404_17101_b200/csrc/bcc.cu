@@ -548,22 +548,43 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
     nxt_out[s] = nx;
 }
 
-__global__ void k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
-                           const u32* __restrict__ HEAD, const Ctr* ctr,
-                           const u32* __restrict__ SUFFIX, uint2* HABW, u32* TA) {
+constexpr int LR_T = 256;
+
+__global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT,
+                                                   const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
+                                                   const Ctr* ctr, const u32* __restrict__ SUFFIX, uint2* HABW,
+                                                   u32* TA) {
+    __shared__ __align__(16) u32 lr_buf[LR_T * 8];
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const TourInfo t = tour_info(ctr, n);
     u32 x;
     if (!ruler_start(s, ns - 1, t, HAB, HEAD, x)) return;
-    u32 pos = t.len - SUFFIX[s];
+    const u32 pos0 = t.len - SUFFIX[s];
+    u32 pos = pos0;
+    // TA[pos] = arc, staged per thread so that whole 32-byte sectors (8 positions, aligned)
+    // are written at once: with ~8M walkers in flight a sector written 4 bytes at a time
+    // leaves L2 half-filled and costs a read-modify-write in HBM
+    u32* buf = lr_buf + threadIdx.x * 8;
     do {
         u32 nx = __ldg(NEXT + (x ^ 1u));   // issue the chain load first
         reinterpret_cast<u32*>(HABW + 2 * (i64)(x >> 1) + 1)[x & 1u] = pos;   // position of arc x
-        TA[pos] = x;
+        buf[pos & 7u] = x;
+        if ((pos & 7u) == 7u) {
+            if (pos - 7u >= pos0) {
+                const uint4* b4 = reinterpret_cast<const uint4*>(buf);
+                uint4* d = reinterpret_cast<uint4*>(TA + (pos - 7u));
+                d[0] = b4[0];
+                d[1] = b4[1];
+            } else {
+                for (u32 q = pos0; q <= pos; ++q) TA[q] = buf[q & 7u];   // this walker's head sector
+            }
+        }
         ++pos;
         x = nx;
     } while (x != PG_INV && (x & (LR_K - 1)) != 0);
+    // the unfinished last sector (possibly also the first): positions [max(pos & ~7, pos0), pos)
+    for (u32 q = (pos & ~7u) > pos0 ? (pos & ~7u) : pos0; q < pos; ++q) TA[q] = buf[q & 7u];
 }
 
 // preorder pass over tour positions, fused into a decoupled-look-back scan of the
