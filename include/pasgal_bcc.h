@@ -127,6 +127,11 @@ int pasgal_csr_validate(const pasgal_csr_t* g, void* workspace, size_t workspace
  * for both, untouched in between. */
 int pasgal_csr_validate_begin(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream);
 int pasgal_csr_validate_end(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, void* stream);
+/* The symmetry check of _end without waiting: queued on `stream`, the final status is
+ * written to *status (a DEVICE int32) when it completes.  For pipelines that keep several
+ * graphs in flight (one workspace per graph in flight). */
+int pasgal_csr_validate_check(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, int32_t* status,
+                              void* stream);
 
 /* Workspace for pasgal_csr_validate: 4 bytes per slot (one bucketed 8-byte key per run of
  * "up" slots, at most m/2 of them) plus ~8 KB per CTA of histograms -- O(m), like the

@@ -64,6 +64,7 @@ SIGNATURES = {
     "pasgal_csr_validate": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
     "pasgal_csr_validate_begin": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
     "pasgal_csr_validate_end": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP]),
+    "pasgal_csr_validate_check": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _SZ, _VP, _VP]),
     "pasgal_csr_build_temp_bytes": (_SZ, [_I64, _I64]),
     "pasgal_csr_from_keys": (_INT, [_I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "pasgal_gen_grid_temp_bytes": (_SZ, [_I64, _I64]),

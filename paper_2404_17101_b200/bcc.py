@@ -80,15 +80,17 @@ class _PendingValidation:
         _lib.check(st, "validate")
 
 
-def _validate_begin(offsets, targets):
+def _validate_begin(offsets, targets, ws=None, side=None):
     """Run the blocking streaming checks now (ranges, row order, up/down balance: after
     this the CSR is safe for FAST-BCC); the symmetry check is the returned object's
     finish().  Raises at once on an early failure."""
     lib = _lib.load()
     dev = offsets.device
     n, m = offsets.shape[0] - 1, targets.shape[0]
-    ws = _workspace(dev, validate_workspace_bytes(n, m), kind="validate")
-    side = _side_stream(dev)
+    if ws is None:
+        ws = _workspace(dev, validate_workspace_bytes(n, m), kind="validate")
+    if side is None:
+        side = _side_stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))        # the CSR's H2D copies
     csr = _csr_struct(offsets, targets)
     st = lib.pasgal_csr_validate_begin(ctypes.byref(csr), _vp(ws), ws.numel(), ctypes.c_void_p(side.cuda_stream))

@@ -1249,6 +1249,7 @@ __global__ void __launch_bounds__(WCH_BLOCK) k_val_pass(const i64* __restrict__ 
                                                         Ctr* ctr, unsigned long long* cnt, u32* hist,
                                                         const u32* __restrict__ base, u64* __restrict__ keys) {
     __shared__ u32 s_bin[VAL_BINS];
+    if (SCATTER && cnt[0] != cnt[1]) return;   // unbalanced: failed already, and keys could exceed m/2
     for (int i = threadIdx.x; i < VAL_BINS; i += WCH_BLOCK)
         s_bin[i] = SCATTER ? base[(i64)i * gridDim.x + blockIdx.x] : 0u;
     __syncthreads();
@@ -1331,13 +1332,8 @@ struct ValBaseStore {
     __device__ __forceinline__ void operator()(i64 i, u32 ex, u32) const { b[i] = ex; }
 };
 
-// One key per thread: row w must hold exactly c copies of u (c = 1 unless the key is
-// flagged, then c is re-counted in row u).
-__global__ void k_val_check(const i64* __restrict__ off, const int32_t* __restrict__ tgt, const u64* __restrict__ keys,
-                            i64 nkeys, Ctr* ctr) {
-    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nkeys) return;
-    const u64 kv = keys[i];
+__device__ __forceinline__ void val_check_key(const i64* __restrict__ off, const int32_t* __restrict__ tgt, u64 kv,
+                                              Ctr* ctr) {
     const int32_t u = (int32_t)(u32)kv, w = (int32_t)((u32)(kv >> 32) & 0x7FFFFFFFu);
     const i64 ws = off[w], we = off[(i64)w + 1];
     const i64 q = lower_bound_row(tgt, ws, we, u);
@@ -1356,6 +1352,19 @@ __global__ void k_val_check(const i64* __restrict__ off, const int32_t* __restri
 static inline unsigned val_grid(i64 m) {
     unsigned b = chunk_blocks(m);
     return b < (unsigned)VAL_GRID ? b : (unsigned)VAL_GRID;
+}
+
+
+// One key per thread (grid-stride; the key count is read on the device, so the check can
+// be queued without a host round trip): row w must hold exactly c copies of u (c = 1
+// unless the key is flagged, then c is re-counted in row u).  Runs only when the counts
+// balance (cnt[0] == cnt[1]); otherwise the streaming half already failed.
+__global__ void k_val_check(const i64* __restrict__ off, const int32_t* __restrict__ tgt, const u64* __restrict__ keys,
+                            const unsigned long long* __restrict__ cnt, Ctr* ctr) {
+    if (cnt[0] != cnt[1]) return;
+    const i64 nkeys = (i64)cnt[2];
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nkeys; i += (i64)gridDim.x * blockDim.x)
+        val_check_key(off, tgt, keys[i], ctr);
 }
 
 struct ValWs {
@@ -1730,35 +1739,50 @@ int csr_validate_begin(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cud
     return PASGAL_OK;
 }
 
-// Validation, second half: the bucketed symmetry check (scan, key scatter, check),
-// launched on `st` and waited for; the final status.  The caller may order it after other
-// work (FAST-BCC) with an event, so it runs while the labels are copied out.
-int csr_validate_end(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+__global__ void k_val_status(const Ctr* ctr, int32_t* status) {
+    const u32 e = ctr->verr;
+    *status = (e & VERR_RANGE) ? PASGAL_ERANGE : (e & VERR_UNSORTED) ? PASGAL_EUNSORTED
+            : (e & VERR_NOTSYM) ? PASGAL_ENOTSYM : PASGAL_OK;
+}
+
+// Validation, second half, asynchronous: the bucketed symmetry check (scan, key scatter,
+// check) is queued on `st` and its final status written to *status (device int32).  No
+// host synchronisation, so the caller can order it after other work (FAST-BCC) with an
+// event and let it run while the labels are copied out.
+int csr_validate_check(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, int32_t* status, cudaStream_t st) {
     const i64 n = g->n, m = g->m_slots;
     ValWs v;
     if (ws_bytes < carve_val(v, nullptr, n, m)) return PASGAL_EWORKSPACE;
     carve_val(v, (char*)ws_ptr, n, m);
     if (m > 0 && n > 0) {
-        unsigned long long c[3];
-        PG_CUDA_TRY(cudaMemcpyAsync(c, v.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
-        PG_CUDA_TRY(cudaStreamSynchronize(st));
-        const i64 nkeys = (i64)c[2];
         const unsigned grid = val_grid(m);
-        const int B = 256;
-        if (nkeys > 0 && c[0] == c[1]) {
-            const i64 nh = (i64)VAL_BINS * grid;
-            PG_CUDA_TRY(launch_scan<u32>(nh, v.SCAN, 0u, SumOp(), ValHistLoad{v.HIST}, ValBaseStore{v.BASE},
-                                         (u32*)nullptr, st));
-            k_val_pass<true><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, val_shift(n), v.ctr,
-                                                          v.cnt, nullptr, v.BASE, v.KEYS);
-            k_val_check<<<nblk(nkeys, B), B, 0, st>>>(g->offsets, g->targets, v.KEYS, nkeys, v.ctr);
-            PG_LAUNCH_CHECK();
-        }
+        const i64 nh = (i64)VAL_BINS * grid;
+        PG_CUDA_TRY(launch_scan<u32>(nh, v.SCAN, 0u, SumOp(), ValHistLoad{v.HIST}, ValBaseStore{v.BASE},
+                                     (u32*)nullptr, st));
+        k_val_pass<true><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, val_shift(n), v.ctr, v.cnt,
+                                                      nullptr, v.BASE, v.KEYS);
+        // one thread per possible key (<= m/2; the true count is read on the device): a
+        // grid-stride loop over 8 CTAs per SM ran 231 ms instead of 148 at RMAT 2^28
+        k_val_check<<<nblk(m / 2 > 0 ? m / 2 : 1, 256), 256, 0, st>>>(g->offsets, g->targets, v.KEYS, v.cnt, v.ctr);
+        PG_LAUNCH_CHECK();
     }
-    Ctr h;
-    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    k_val_status<<<1, 1, 0, st>>>(v.ctr, status);
+    PG_LAUNCH_CHECK();
+    return PASGAL_OK;
+}
+
+// Validation, second half, blocking: the check above, waited for; the final status.
+int csr_validate_end(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
+    ValWs v;
+    if (ws_bytes < carve_val(v, nullptr, g->n, g->m_slots)) return PASGAL_EWORKSPACE;
+    carve_val(v, (char*)ws_ptr, g->n, g->m_slots);
+    int32_t* status = reinterpret_cast<int32_t*>(v.cnt + 3);   // spare counter word
+    int s = csr_validate_check(g, ws_ptr, ws_bytes, status, st);
+    if (s) return s;
+    int32_t h = 0;
+    PG_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof h, cudaMemcpyDeviceToHost, st));
     PG_CUDA_TRY(cudaStreamSynchronize(st));
-    return val_status(h.verr);
+    return h;
 }
 
 int csr_validate(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {

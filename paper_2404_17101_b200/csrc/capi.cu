@@ -26,6 +26,7 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
 int csr_validate_begin(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
 int csr_validate_end(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
+int csr_validate_check(const pasgal_csr_t* g, void* ws, size_t ws_bytes, int32_t* status, cudaStream_t st);
 size_t gen_grid_temp_bytes(i64 rows, i64 cols);
 int gen_grid(i64 rows, i64 cols, u64 seed, u64 thr, int keep_all, i64* off, int32_t* tgt, i64* m_dev, void* temp,
              size_t temp_bytes, cudaStream_t st);
@@ -113,6 +114,15 @@ int pasgal_csr_validate_end(const pasgal_csr_t* g, void* workspace, size_t works
     if (s) return s;
     if (!workspace) return PASGAL_EWORKSPACE;
     return pg::csr_validate_end(g, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int pasgal_csr_validate_check(const pasgal_csr_t* g, void* workspace, size_t workspace_bytes, int32_t* status,
+                              void* stream) {
+    int s = check_csr(g);
+    if (s) return s;
+    if (!workspace) return PASGAL_EWORKSPACE;
+    if (!status) return PASGAL_EINVAL;
+    return pg::csr_validate_check(g, workspace, workspace_bytes, status, (cudaStream_t)stream);
 }
 
 size_t pasgal_csr_validate_workspace_bytes(int64_t n, int64_t m_slots) {

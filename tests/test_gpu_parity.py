@@ -319,3 +319,26 @@ def test_hub_shapes_match_oracle():
     for nv, s, t in shapes:
         dg = pg.symmetrize_edges(nv, s, t)
         _parity_device_graph(dg)
+
+
+def test_pipeline_matches_single_calls_and_raises_in_order():
+    """BccPipeline (H2D / BCC / D2H of consecutive graphs overlapped) returns exactly what
+    bcc(g) returns for each graph, and a non-symmetric graph raises the reference's error
+    when its result is reached."""
+    graphs = [pg.Graph(c.offsets, c.targets) for c in golden_io.kats()]
+    dg = pg.make_config("c2")
+    graphs.insert(3, dg.to_host())
+    graphs.append(dg.to_host())
+    n_seen = 0
+    for r, g in zip(pg.BccPipeline().run(graphs), graphs):   # compared before the next result
+        ref = pg.bcc(g)
+        assert r.bcc_count == ref.bcc_count
+        assert np.array_equal(r.articulation, ref.articulation)
+        assert np.array_equal(pg.canonical_edge_partition(g, r), pg.canonical_edge_partition(g, ref))
+        n_seen += 1
+    assert n_seen == len(graphs)
+    bad = pg.Graph(np.array([0, 1, 1, 2], dtype=np.int64), np.array([1, 0], dtype=np.uint32))
+    it = pg.BccPipeline().run([graphs[0], bad, graphs[1]])
+    next(it)
+    with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
+        next(it)
