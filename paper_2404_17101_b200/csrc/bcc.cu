@@ -1705,6 +1705,44 @@ static int val_shift(i64 n) {
     return bits > VAL_BINS_LB ? bits - VAL_BINS_LB : 0;
 }
 
+// Small results of the streaming checks go to the host through mapped pinned memory
+// written by a one-thread kernel, not cudaMemcpy: a D2H copy of a few bytes queues behind
+// any large D2H on the copy engine (in BccPipeline, the previous graph's 17 GB of labels),
+// which held each graph's BCC back ~185 ms at RMAT 2^28.  One buffer per host thread keeps
+// the library reentrant; a call finishes with it before returning.
+struct ValReadback {
+    unsigned long long verr, up, down, keys;
+};
+
+__global__ void k_val_publish(const Ctr* ctr, const unsigned long long* cnt, volatile ValReadback* h) {
+    h->verr = ctr->verr;
+    h->up = cnt ? cnt[0] : 0ull;
+    h->down = cnt ? cnt[1] : 0ull;
+    h->keys = cnt ? cnt[2] : 0ull;
+}
+
+static cudaError_t val_readback(const Ctr* ctr, const unsigned long long* cnt, cudaStream_t st, ValReadback* out) {
+    thread_local ValReadback* hbuf = nullptr;
+    thread_local ValReadback* dbuf = nullptr;
+    if (!hbuf) {
+        cudaError_t e = cudaHostAlloc((void**)&hbuf, sizeof(ValReadback), cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return e;
+        e = cudaHostGetDevicePointer((void**)&dbuf, hbuf, 0);
+        if (e != cudaSuccess) return e;
+    }
+    k_val_publish<<<1, 1, 0, st>>>(ctr, cnt, dbuf);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+        const volatile ValReadback* v = hbuf;
+        out->verr = v->verr;
+        out->up = v->up;
+        out->down = v->down;
+        out->keys = v->keys;
+    }
+    return e;
+}
+
 // Validation, first half: the streaming checks (ranges, row order, #up == #down, and the
 // bucket histogram of the keys), waited for.  After PASGAL_OK the CSR is safe for
 // FAST-BCC.  A nonzero return is final.
@@ -1719,9 +1757,8 @@ int csr_validate_begin(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cud
     const int B = 256;
     k_validate_offsets<<<nblk(n + 1, B), B, 0, st>>>(n, m, g->offsets, v.ctr);
     PG_LAUNCH_CHECK();
-    Ctr h;
-    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
-    PG_CUDA_TRY(cudaStreamSynchronize(st));
+    ValReadback h;
+    PG_CUDA_TRY(val_readback(v.ctr, nullptr, st, &h));
     if (h.verr & VERR_RANGE) return PASGAL_ERANGE;
     if (m == 0 || n == 0) return PASGAL_OK;
     const i64 nch = num_chunks(m);
@@ -1730,12 +1767,9 @@ int csr_validate_begin(const pasgal_csr_t* g, void* ws_ptr, size_t ws_bytes, cud
     k_val_pass<false><<<grid, WCH_BLOCK, 0, st>>>(g->offsets, g->targets, n, m, v.CROW, val_shift(n), v.ctr, v.cnt,
                                                    v.HIST, nullptr, nullptr);
     PG_LAUNCH_CHECK();
-    unsigned long long c[3];
-    PG_CUDA_TRY(cudaMemcpyAsync(&h, v.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, st));
-    PG_CUDA_TRY(cudaMemcpyAsync(c, v.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
-    PG_CUDA_TRY(cudaStreamSynchronize(st));
-    if (h.verr) return val_status(h.verr);
-    if (c[0] != c[1]) return PASGAL_ENOTSYM;
+    PG_CUDA_TRY(val_readback(v.ctr, v.cnt, st, &h));
+    if (h.verr) return val_status((u32)h.verr);
+    if (h.up != h.down) return PASGAL_ENOTSYM;
     return PASGAL_OK;
 }
 

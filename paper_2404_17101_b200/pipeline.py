@@ -58,12 +58,13 @@ class _Slot:
 class BccPipeline:
     """Streamed ``bcc(g)`` over an iterable of host graphs (see the module docstring)."""
 
-    def __init__(self, device="cuda", validate=True, seed=0):
+    def __init__(self, device="cuda", validate=True, seed=0, trace=None):
         self.dev = torch.device(device)
         if self.dev.index is None:
             self.dev = torch.device("cuda", torch.cuda.current_device())
         self.validate = validate
         self.seed = seed
+        self.trace = trace      # optional list: (graph, what, timing event) for tools/pipeline_probe.py
         self.copy_in = torch.cuda.Stream(self.dev)
         self.copy_out = torch.cuda.Stream(self.dev)
         self.compute = _priority_stream(self.dev)
@@ -77,6 +78,12 @@ class BccPipeline:
         self.vside = [torch.cuda.Stream(self.dev, priority=0), torch.cuda.Stream(self.dev, priority=0)]
         self.vslot = [_Slot(), _Slot()]
 
+    def _mark(self, i, what, stream):
+        if self.trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.trace.append((i, what, e))
+
     def _h2d(self, i, g):
         s = i % 2
         off, tgt = _host_csr(g)
@@ -86,6 +93,7 @@ class BccPipeline:
         with torch.cuda.stream(self.copy_in):
             if self.in_free[s] is not None:
                 self.copy_in.wait_event(self.in_free[s])
+            self._mark(i, "h2d_start", self.copy_in)
             off_d = self.din[s].get("off", n + 1, torch.int64, self.dev)
             tgt_d = self.din[s].get("tgt", m, torch.int32, self.dev)
             off_d.copy_(torch.from_numpy(off), non_blocking=True)
@@ -93,6 +101,7 @@ class BccPipeline:
                 tgt_d.copy_(torch.from_numpy(tgt), non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.copy_in)
+            self._mark(i, "h2d_end", self.copy_in)
         return dict(i=i, n=n, m=m, off=off_d, tgt=tgt_d, h2d=ev)
 
     def _compute(self, job):
@@ -101,6 +110,7 @@ class BccPipeline:
         cs = self.compute
         cs.wait_event(job["h2d"])
         with torch.cuda.stream(cs):
+            self._mark(job["i"], "compute_start", cs)
             pending = None
             if self.validate:
                 vws = self.vslot[s].get("ws", validate_workspace_bytes(n, m), torch.uint8, self.dev)
@@ -112,6 +122,7 @@ class BccPipeline:
             cnt = self.dout[s].get("cnt", 1, torch.int64, self.dev)
             ws = _workspace(self.dev, workspace_bytes(n, m))
             lib = _lib.load()
+            self._mark(job["i"], "bcc_start", cs)
             csr = _lib.PasgalCsr(n, m, job["off"].data_ptr(), job["tgt"].data_ptr() if m else 0)
             out = _lib.PasgalBccOut(lab.data_ptr() if m else 0, bits.data_ptr() if n else 0, cnt.data_ptr(), 0, 0, 0)
             st = lib.pasgal_bcc(ctypes.byref(csr), ctypes.byref(out), _vp(ws), ws.numel(),
@@ -122,27 +133,31 @@ class BccPipeline:
             art = articulation_bytes_device(bits, n)
             done = torch.cuda.Event()
             done.record(cs)
+            self._mark(job["i"], "bcc_end", cs)
         # the symmetry check, queued behind the BCC kernels (it overlaps the D2H below); its
         # status word reaches pinned host memory on the same side stream
         check = None
         if pending is not None:
             vs = self.vside[s]
             vs.wait_event(done)
-            st_d = self.vslot[s].get("status", 1, torch.int32, self.dev)
+            # the status goes straight to pinned (mapped, under unified addressing) host memory:
+            # a 4-byte D2H copy would queue behind the next graph's label copy on the copy
+            # engine and hold the input slot (and so the next H2D) ~0.5 s
             st_h = self.vslot[s].get("status_h", 1, torch.int32, "cpu", pin=True)
             with torch.cuda.stream(vs):
                 rc = lib.pasgal_csr_validate_check(ctypes.byref(pending.csr), _vp(pending.ws), pending.ws.numel(),
-                                                   _vp(st_d), ctypes.c_void_p(vs.cuda_stream))
+                                                   _vp(st_h), ctypes.c_void_p(vs.cuda_stream))
                 _lib.check(rc, "validate")
-                st_h.copy_(st_d, non_blocking=True)
                 check = torch.cuda.Event()
                 check.record(vs)
+                self._mark(job["i"], "check_end", vs)
             pending.keep = None
             job.update(status_h=st_h)
         # D2H on the copy-out stream
         co = self.copy_out
         co.wait_event(done)
         with torch.cuda.stream(co):
+            self._mark(job["i"], "d2h_start", co)
             hl = self.hout[s].get("lab", m, torch.int32, "cpu", pin=True)
             ha = self.hout[s].get("art", n, torch.uint8, "cpu", pin=True)
             hc = self.hout[s].get("cnt", 1, torch.int64, "cpu", pin=True)
@@ -153,6 +168,7 @@ class BccPipeline:
             hc.copy_(cnt, non_blocking=True)
             d2h = torch.cuda.Event()
             d2h.record(co)
+            self._mark(job["i"], "d2h_end", co)
         self.out_free[s] = d2h
         self.in_free[s] = check if check is not None else done
         job.update(check=check, d2h=d2h, hl=hl, ha=ha, hc=hc)
@@ -171,13 +187,22 @@ class BccPipeline:
         """Yield BccLabels for each graph in order.  A yielded result's arrays are views of
         pinned buffers that are overwritten once the next result is requested: copy them to
         keep them."""
-        prev = None
-        for i, g in enumerate(graphs):
+        it = iter(graphs)
+
+        def h2d(i):
+            g = next(it, None)
+            if g is None:
+                return None
             if isinstance(g, DeviceGraph):
                 raise TypeError("BccPipeline takes host graphs; use bcc_device for device-resident CSRs")
-            job = self._compute(self._h2d(i, g))   # H2D(i) overlaps D2H(i-1); BCC(i) queued
+            return self._h2d(i, g)
+
+        nxt, prev, i = h2d(0), None, 0
+        while nxt is not None:
+            job = self._compute(nxt)        # waits for H2D(i) + the streaming checks; queues BCC(i), D2H(i)
+            nxt = h2d(i + 1)                # H2D(i+1) right away: it overlaps BCC(i) and the D2Hs
             if prev is not None:
-                yield self._finish(prev)            # i-1: symmetry check, then its D2H
-            prev = job
+                yield self._finish(prev)    # i-1: symmetry check status, its D2H
+            prev, i = job, i + 1
         if prev is not None:
             yield self._finish(prev)
