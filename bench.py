@@ -491,6 +491,18 @@ def run_e2e(args, off_h, tgt_h, dev, n, m):
     # pipelined: the same per-step copies and work, consecutive steps overlapped
     pg.release_workspace()
     torch.cuda.empty_cache()
+    need = 2 * (4 * m + n + 8)                          # two pinned output slots per rank
+    world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = None
+    if avail is not None and avail < 1.5 * world * need:
+        out["pipelined"] = {"unavailable": f"host memory: {world} ranks x {need / 1e9:.1f} GB of pinned output "
+                                           f"slots exceed 2/3 of the {avail / 1e9:.0f} GB available"}
+        return out
     try:
         psteps = max(6, steps + 1)
         pipe = pg.BccPipeline(device=dev)
