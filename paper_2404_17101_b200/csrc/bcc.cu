@@ -865,7 +865,7 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 #define PG_NSAMPLE2 1
 #endif
 #ifndef PG_SCAN2
-#define PG_SCAN2 3
+#define PG_SCAN2 2
 #endif
 #ifndef PG_SAMPLE2_MODE
 #define PG_SAMPLE2_MODE 1
