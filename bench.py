@@ -433,6 +433,16 @@ def run_batch(args, rank, world, local):
     total_ms = e0.elapsed_time(e1)
     mu = sum(g.m // 2 for g in graphs) * args.steps
     total_ms, edges = reduce_over_ranks(total_ms, mu, dev)
+    # per-instance canonical checksums (outside the timed region), and on rank 0
+    # the first --verify instances re-run by the C oracle on the host threads
+    sums = []
+    for g in graphs:
+        r = pg.bcc_device(g.offsets, g.targets, canonical=True, out=outs[0], workspace=wss[0])
+        sums.append(pg.canonical_checksum_device(r.edge_label[:g.m], r.artic_bits[:(g.n + 31) // 32], r.bcc_count))
+    verified = None
+    if rank == 0 and args.verify > 0:
+        verified = verify_instances([graphs[i] for i in range(min(args.verify, len(graphs)))],
+                                    sums[:args.verify])
     if rank == 0:
         line = {
             "metric": METRIC, "value": edges / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
@@ -444,11 +454,44 @@ def run_batch(args, rank, world, local):
                        "instances_per_s": args.instances * args.steps / (total_ms / 1e3),
                        "l2": "inputs larger than L2 (batch of 64 x 295 MB CSR)"},
             "gpu_launches": launches, "clocks": clocks,
+            "checksums": {"instances": [mine[i] + 1 for i in range(len(sums))][:8],
+                          "bcc_count_art_hash": [list(map(str, c)) for c in sums[:8]],
+                          "rule": "(bcc_count, articulation points, sum canon[s]*(((s*0x9E3779B1) mod 2^32)|1) mod 2^64)"},
+            "verified": verified,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def verify_instances(graphs, sums):
+    """Re-run the first instances with the C oracle (one host thread each) and compare the
+    canonical checksums (per-instance checksums against the oracle)."""
+    import numpy as np
+
+    import oracle
+    import paper_2404_17101_b200 as pg
+
+    oracle.build()
+    host = [(g.offsets.cpu().numpy(), g.targets.cpu().numpy().view(np.uint32)) for g in graphs]
+    got = [None] * len(host)
+
+    def work(i):
+        off, tgt = host[i]
+        r = oracle.bcc_hopcroft_tarjan(off, tgt)
+        canon = oracle.canonical_min_eid(off, tgt, r.edge_label)
+        got[i] = pg.canonical_checksum(canon, r.articulation, r.bcc_count)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(host))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return {"instances": len(host), "match": all(a == tuple(b) for a, b in zip(got, sums)),
+            "host_threads": len(host), "seconds": round(time.perf_counter() - t0, 1),
+            "checker": "oracle/bcc_oracle.c (C restatement of bcc_hopcroft_tarjan) + canonical_min_eid"}
 
 
 def run_e2e(args, off_h, tgt_h, dev, n, m):
@@ -534,6 +577,7 @@ def main():
     ap.add_argument("--config", default="c5a", choices=["c1", "c2", "c3", "c4", "c5a", "c5b"])
     ap.add_argument("--instances", type=int, default=64, help="c5b: batch size (grid instances)")
     ap.add_argument("--streams", type=int, default=4, help="c5b: concurrent instances per GPU")
+    ap.add_argument("--verify", type=int, default=8, help="c5b: instances re-checked by the C oracle on rank 0")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0, help="sampling seed of the BCC call")
     ap.add_argument("--e2e-steps", type=int, default=2)

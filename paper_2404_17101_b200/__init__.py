@@ -5,10 +5,10 @@ Drop-in for the reference package's biconnectivity entry point
 CUDA kernels behind a C-ABI (include/pasgal_bcc.h).  See DESIGN.md.
 """
 
-from .results import BccLabels, canonical_edge_partition, canonical_relabel, min_eid_to_partition
+from .results import BccLabels, canonical_checksum, canonical_edge_partition, canonical_relabel, min_eid_to_partition
 from .graph import (CONFIGS, DeviceGraph, Graph, csr_from_keys, gen_grid, gen_knn, gen_rmat, make_config,
                     symmetrize_edges)
-from .bcc import (DeviceBcc, HostBuffers, canonicalize_device, connected_components, connected_components_device,
+from .bcc import (DeviceBcc, HostBuffers, canonical_checksum_device, canonicalize_device, connected_components, connected_components_device,
                   same_partition_device)
 from .bcc import articulation_bytes_device, bcc, bcc_device, release_workspace, unpack_articulation, validate_device, validate_workspace_bytes, workspace_bytes
 
@@ -19,9 +19,9 @@ from .bfs import UNREACHED, DistanceArray, GraphStats, bfs, eccentricities, esti
 __all__ = [
     "GraphFormatError", "load_adj", "load_bin", "save_adj", "save_bin",
     "BccPipeline", "UNREACHED", "DistanceArray", "GraphStats", "bfs", "eccentricities", "estimate_diameter",
-    "BccLabels", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
+    "BccLabels", "canonical_checksum", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
     "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",
-    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonicalize_device", "same_partition_device", "articulation_bytes_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
+    "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonical_checksum_device", "canonicalize_device", "same_partition_device", "articulation_bytes_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",
     "validate_device", "validate_workspace_bytes", "workspace_bytes",
 ]
 

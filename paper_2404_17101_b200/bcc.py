@@ -252,6 +252,23 @@ def canonicalize_device(offsets, targets, labels, label_bound=None):
     return out
 
 
+def canonical_checksum_device(canon_labels, artic_bits, bcc_count):
+    """Device twin of results.canonical_checksum: canon_labels is the int32 storage of the
+    canonical uint32 labels (bcc_device(..., canonical=True).edge_label), artic_bits the
+    device bitmap, bcc_count the device count.  Integer products and sums wrap mod 2^64 on
+    the device exactly as in the host's uint64 arithmetic."""
+    m = canon_labels.shape[0]
+    lab = canon_labels.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    s = torch.arange(m, dtype=torch.int64, device=canon_labels.device)
+    w = ((s * 0x9E3779B1) & 0xFFFFFFFF) | 1
+    h = int((lab * w).sum().item()) % (1 << 64) if m else 0
+    bits = artic_bits.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    nart = 0
+    for k in range(32):                      # popcount over the bitmap words
+        nart += int(((bits >> k) & 1).sum().item())
+    return int(bcc_count.item()), nart, h
+
+
 def same_partition_device(offsets, targets, labels_a, labels_b, label_bound=None):
     """True iff two per-slot labellings induce the same edge partition (device comparator)."""
     a = canonicalize_device(offsets, targets, labels_a, label_bound)

@@ -102,3 +102,18 @@ def min_eid_to_partition(g, canon_labels):
     ids = np.asarray(canon_labels)[up].astype(np.int64)
     _, dense = np.unique(ids, return_inverse=True)
     return dense.reshape(-1).astype(np.int64)
+
+
+_CHK_MUL = 0x9E3779B1
+
+
+def canonical_checksum(canon_labels, articulation, bcc_count):
+    """Order-independent run checksum: (bcc_count, number of
+    articulation points, sum over slots of canon[s] * w(s) mod 2^64) with canon the
+    min-undirected-edge-id labels (uint32, 0xFFFFFFFF for self-loops) and the odd weight
+    w(s) = ((s * 0x9E3779B1) mod 2^32) | 1.  canonical_checksum_device is its device twin."""
+    lab = np.asarray(canon_labels).view(np.uint32).astype(np.uint64)
+    s = np.arange(lab.shape[0], dtype=np.uint64)
+    w = ((s * np.uint64(_CHK_MUL)) & np.uint64(0xFFFFFFFF)) | np.uint64(1)
+    h = int((lab * w).sum(dtype=np.uint64)) if lab.shape[0] else 0
+    return int(bcc_count), int(np.count_nonzero(articulation)), h

@@ -342,3 +342,22 @@ def test_pipeline_matches_single_calls_and_raises_in_order():
     next(it)
     with pytest.raises(ValueError, match="^biconnectivity requires a symmetric graph$"):
         next(it)
+
+
+def test_canonical_checksum_device_equals_host():
+    dg = pg.make_config("c1")
+    r = pg.bcc_device(dg.offsets, dg.targets, canonical=True)
+    dev_sum = pg.canonical_checksum_device(r.edge_label, r.artic_bits, r.bcc_count)
+    off = dg.offsets.cpu().numpy()
+    tgt = dg.targets.cpu().numpy().view(np.uint32)
+    ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+    host_sum = pg.canonical_checksum(oracle.canonical_min_eid(off, tgt, ref.edge_label), ref.articulation,
+                                     ref.bcc_count)
+    assert dev_sum == host_sum
+    kat = [c for c in golden_io.kats() if "loop" in c.name or c.name == "bowtie"][0]
+    g = pg.Graph(kat.offsets, kat.targets)
+    r = pg.bcc_device(torch.from_numpy(kat.offsets).cuda(), torch.from_numpy(kat.targets.view(np.int32)).cuda(),
+                      canonical=True)
+    ref = oracle.bcc_hopcroft_tarjan(g.offsets, g.targets)
+    assert pg.canonical_checksum_device(r.edge_label, r.artic_bits, r.bcc_count) == pg.canonical_checksum(
+        oracle.canonical_min_eid(g.offsets, g.targets, ref.edge_label), ref.articulation, ref.bcc_count)

@@ -162,3 +162,15 @@ def test_generator_thresholds_match_oracle_twin():
     assert rmat_thresholds(0.57, 0.19, 0.19) == oracle.rmat_thresholds(0.57, 0.19, 0.19)
     for n in [1, 7, 100, 1 << 20, 1 << 25]:
         assert knn_gbits(n) == oracle.knn_gbits(n)
+
+
+def test_canonical_checksum_rule():
+    from paper_2404_17101_b200.results import canonical_checksum
+
+    lab = np.array([0, 0, 2, 0xFFFFFFFF, 2], dtype=np.uint32)
+    art = np.array([False, True, True])
+    c, a, h = canonical_checksum(lab, art, 2)
+    assert (c, a) == (2, 2)
+    w = [((s * 0x9E3779B1) % (1 << 32)) | 1 for s in range(5)]
+    assert h == sum(int(x) * y for x, y in zip(lab, w)) % (1 << 64)
+    assert canonical_checksum(lab[::-1].copy(), art, 2)[2] != h      # slot order matters
