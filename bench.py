@@ -45,7 +45,7 @@ KERNEL_BYTES = {
     # k_labels: per slot target 4 + (first,comp)[w] 8 + label write 4; per vertex offsets 8 + (first,comp)[u] 8
     "labels": lambda n, m: 16 * m + 16 * n,
 }
-KERNEL_NAMES = {"tags": "k_tags", "labels": "k_labels"}
+KERNEL_NAMES = {"tags": "k_tags_blk", "labels": "k_labels"}
 
 
 def assign_instances(n_instances, rank, world):

@@ -16,7 +16,7 @@
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
 //   S3 rooting    k_arc_link, k_arc_close (root chain, isolated slots), ruling-set list ranking (k_lr_walk1,
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
-//   S4 tags       k_tags (per slot), k_rmq_block/level/query (blocked sparse table)
+//   S4 tags       k_tags_blk (per slot, blocked chunks), k_rmq_block/level/query (sparse table)
 //   S5 Last-CC    k_cc2_local / k_cc2_tree (non-fence tree edges, preorder blocks in shared
 //                 memory first), k_cc2_sample, k_giant, k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
@@ -32,9 +32,6 @@
 namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
-#ifndef PG_TAGS_MINB
-#define PG_TAGS_MINB 8
-#endif
 #ifndef PG_LABELS_MINB
 #define PG_LABELS_MINB 8
 #endif
@@ -661,19 +658,6 @@ __global__ void k_vertex_first(i64 n, const uint2* __restrict__ FL, const u32* _
 // --------------------------------------------------------------------------
 // S4: tags  w1/w2[first[v]] = min/max(first[v], first[u] for all neighbours u)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ void warp_seg_minmax(int r, u32& mn, u32& mx, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int ro = __shfl_down_sync(0xFFFFFFFFu, r, o);
-        u32 a = __shfl_down_sync(0xFFFFFFFFu, mn, o);
-        u32 b = __shfl_down_sync(0xFFFFFFFFu, mx, o);
-        if (lane + o < 32 && ro == r) {
-            mn = a < mn ? a : mn;
-            mx = b > mx ? b : mx;
-        }
-    }
-}
-
 __device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u32 mn, u32 mx, bool atomic) {
     u32 f = __ldg(FIRST + row);
     if (atomic) {
@@ -684,70 +668,78 @@ __device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u
     }
 }
 
-// The row running past a window edge carries its min/max to the next window of the chunk
-// in registers (warp-uniform), so a long row costs one atomic pair per 256-slot chunk
-// instead of one per window.  A row is stored without atomics when it begins and ends in
-// this chunk; a row that may extend into a neighbouring chunk uses atomics.
-__global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                                                    i64 n, i64 m, const u32* __restrict__ crow,
-                                                    const u32* __restrict__ FIRST, uint2* W) {
+// Blocked-chunk k_tags (wchunk.cuh): lane l reduces its 8 consecutive slots sequentially;
+// a row wholly inside the lane is stored at once, and rows crossing lanes are combined by
+// one segmented warp scan.  Rows that began before the chunk or continue after it use
+// atomics.  The FIRST gathers themselves run in the strided layout (one instruction covers
+// 32 consecutive slots: the sorted hub rows' targets share lines) and are transposed
+// through shared memory.  It replaced a per-32-slot-window design (row search, segment
+// mask, two redux and a carry per window) that was instruction-bound: C3 tags 0.50 ->
+// 0.21 ms; C5a is gather-bound and unchanged (36.7 ms).
+#ifndef PG_TAGS_MINB
+#define PG_TAGS_MINB 6
+#endif
+__global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64* __restrict__ off,
+                                                                const int32_t* __restrict__ tgt, i64 n, i64 m,
+                                                                const u32* __restrict__ crow,
+                                                                const u32* __restrict__ FIRST, uint2* W) {
+    __shared__ BlkSmem smem[WCH_BLOCK / 32];
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
+    BlkSmem& sm = smem[threadIdx.x >> 5];
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
-    u32 fw[WCH_U];
+    const i64 sl = s0 + BLK_SPL * lane;
+    u32 fw[BLK_SPL];
+    {
+        u32 g[WCH_U];   // strided: one gather instruction covers 32 consecutive slots
+        wc_load(tgt, m, c, lane, g);
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        i64 s = s0 + 32 * k + lane;
-        fw[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
+        for (int k = 0; k < WCH_U; ++k)
+            if (s0 + 32 * k + lane < s1) g[k] = __ldg(FIRST + g[k]);
+        blk_transpose(sm, lane, g, fw);
     }
+    const BlkRows br = blk_rows(off, n, s0, s1, crow[c], lane, sm);
+    const bool hstart = br.mb & 1u;
+    u32 r = br.r_first;
+    u32 mn = PG_INV, mx = 0, hmn = PG_INV, hmx = 0;
+    bool in_head = true;
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        i64 s = s0 + 32 * k + lane;
-        if (s < s1) fw[k] = __ldg(FIRST + fw[k]);
-    }
-    u32 cur = crow[c];
-    u32 crw = PG_INV, cmn = PG_INV, cmx = 0;   // carried row and its running min/max
-    bool cbefore = false;                      // carried row began before this chunk
-#pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        const i64 sb = s0 + 32 * k;
-        if (sb >= s1) break;  // warp-uniform
-        const bool valid = sb + lane < s1;
-        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
-        const u32 row = wc_resolve_row(off, n, cur, sb, lane, valid);
-        cur = __shfl_sync(0xFFFFFFFFu, row, 31);
-        const Seg g = wc_segment(row, lane, valid, vm);
-        u32 mn = PG_INV, mx = 0;
-        if (valid) {
-            mn = __reduce_min_sync(g.mask, fw[k]);
-            mx = __reduce_max_sync(g.mask, fw[k]);
+    for (int i = 0; i < BLK_SPL; ++i) {
+        if (i > 0 && (br.mb >> i & 1u)) {        // a row starts at slot i: the current one ended
+            if (in_head) {
+                hmn = mn;
+                hmx = mx;
+                in_head = false;
+                if (hstart) write_tag(W, FIRST, r, mn, mx, false);   // began at p0: complete
+            } else {
+                write_tag(W, FIRST, r, mn, mx, false);               // began and ended in the lane
+            }
+            r = sm.row[BLK_SPL * lane + i];
+            mn = PG_INV;
+            mx = 0;
         }
-        const u32 row0 = __shfl_sync(0xFFFFFFFFu, row, 0);
-        if (crw != PG_INV && crw != row0) {     // carried row ended at the previous window edge
-            if (lane == 0) write_tag(W, FIRST, crw, cmn, cmx, cbefore);
-            crw = PG_INV;
-        }
-        const bool merged = crw != PG_INV;       // then crw == row0: the first segment continues it
-        if (merged && g.lo == 0) {
-            mn = mn < cmn ? mn : cmn;
-            mx = mx > cmx ? mx : cmx;
-        }
-        // began before this chunk: only the first segment of the first window can (unknown,
-        // so assumed), or a merged carry that did
-        const bool before = g.lo == 0 && (merged ? cbefore : k == 0);
-        const bool has_next = sb + 32 < s1;      // window full and more of the chunk follows
-        if (valid && lane == g.lo && !(g.cut_right && has_next))
-            write_tag(W, FIRST, row, mn, mx, before || g.cut_right);
-        if (has_next) {                          // lane 31's segment continues: carry it
-            crw = __shfl_sync(0xFFFFFFFFu, row, 31);
-            cmn = __shfl_sync(0xFFFFFFFFu, mn, 31);
-            cmx = __shfl_sync(0xFFFFFFFFu, mx, 31);
-            cbefore = __shfl_sync(0xFFFFFFFFu, (int)before, 31) != 0;
-        } else {
-            crw = PG_INV;
+        if (sl + i < s1) {
+            mn = fw[i] < mn ? fw[i] : mn;
+            mx = fw[i] > mx ? fw[i] : mx;
         }
     }
+    // mn/mx: the lane's last row, open to the right; scan it across lanes
+    const bool inner = (br.mb & 0xFEu) != 0;
+    u32 cmn = mn, cmx = mx;
+    bool started;
+    blk_seg_scan(lane, hstart || inner, cmn, cmx, started);
+    const u32 pmn = __shfl_up_sync(0xFFFFFFFFu, cmn, 1), pmx = __shfl_up_sync(0xFFFFFFFFu, cmx, 1);
+    const bool pstarted = __shfl_up_sync(0xFFFFFFFFu, (int)started, 1) != 0 && lane > 0;
+    if (inner && !hstart) {                      // head row came from the left and ends here
+        const u32 tmn = lane > 0 && pmn < hmn ? pmn : hmn;
+        const u32 tmx = lane > 0 && pmx > hmx ? pmx : hmx;
+        write_tag(W, FIRST, br.r_first, tmn, tmx, !pstarted);
+    }
+    // the lane's last row ends exactly at the lane's end when the next lane starts a row
+    const bool next_starts = __shfl_down_sync(0xFFFFFFFFu, (int)hstart, 1) != 0;
+    if (lane < 31 && next_starts) write_tag(W, FIRST, r, cmn, cmx, !started);
+    if (lane == 31) write_tag(W, FIRST, r, cmn, cmx, !started || br.last_open);
 }
 
 // --------------------------------------------------------------------------
@@ -1481,7 +1473,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
-    if (w.nch > 0) PG_K(k_tags<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+    if (w.nch > 0) PG_K(k_tags_blk<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));

@@ -30,6 +30,16 @@ inline unsigned chunk_blocks(i64 m) {
     return (unsigned)(b > 0 ? b : 1);
 }
 
+// targets of chunk c (zeros past the end), streaming loads
+__device__ __forceinline__ void wc_load(const int32_t* __restrict__ tgt, i64 m, i64 c, int lane, u32 (&w)[WCH_U]) {
+    const i64 s0 = c * WCH;
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) {
+        const i64 s = s0 + 32 * k + lane;
+        w[k] = s < m ? (u32)__ldcs(tgt + s) : 0u;
+    }
+}
+
 // crow[c] = row containing slot c*WCH (largest r with off[r] <= c*WCH)
 __global__ void k_chunk_rows(const i64* __restrict__ off, i64 n, i64 m, i64 nch, u32* __restrict__ crow) {
     i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -96,6 +106,136 @@ __device__ __forceinline__ Seg wc_segment(u32 row, int lane, bool valid, unsigne
     s.cut_left = s.lo == 0;
     s.cut_right = !after;
     return s;
+}
+
+}  // namespace pg
+
+// --------------------------------------------------------------------------
+// Blocked warp chunks: lane l owns the 8 CONSECUTIVE slots s0 + 8l .. s0 + 8l + 7 of the
+// warp's 256-slot chunk, so a per-row reduction is a sequential loop in the lane plus one
+// segmented warp scan for rows that cross lanes -- instead of a row search, a segment
+// mask and two redux per 32-slot window.  Row starts come from one pass over the
+// chunk's rows (offsets loaded 32 rows at a time): a per-warp 256-bit start mask and the
+// row id at each start position, in shared memory (1 KB + 32 B per warp; no block sync).
+// --------------------------------------------------------------------------
+namespace pg {
+
+constexpr int BLK_SPL = 8;                 // slots per lane
+static_assert(WCH == 32 * BLK_SPL && BLK_SPL == WCH_U, "blocked chunks cover the same 256 slots");
+
+struct BlkSmem {
+    union {
+        u32 row[WCH];             // row id of a nonempty row starting at chunk position p (where the mask is set)
+        u32 xp[WCH + WCH / 32];   // strided -> blocked transpose, padded (conflict-free both ways); dead
+                                  // before blk_rows writes `row`
+    };
+    u32 mask[WCH / 32];
+};
+
+// Values gathered in the strided layout (lane l holds positions 32k + l, so the gathers of
+// one instruction hit consecutive, often line-sharing, targets) handed to the blocked
+// layout (lane l gets positions 8l .. 8l+7).  Padding index p -> p + (p >> 5).
+__device__ __forceinline__ void blk_transpose(BlkSmem& sm, int lane, const u32 (&strided)[WCH_U],
+                                              u32 (&blocked)[BLK_SPL]) {
+    __syncwarp();   // a previous transpose's reads are done before the buffer is rewritten
+#pragma unroll
+    for (int k = 0; k < WCH_U; ++k) sm.xp[32 * k + lane + k] = strided[k];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < BLK_SPL; ++i) {
+        const int p = BLK_SPL * lane + i;
+        blocked[i] = sm.xp[p + (p >> 5)];
+    }
+}
+
+struct BlkRows {
+    u32 mb;            // bit i: a nonempty row starts at slot p0 + i of this lane
+    u32 r_first;       // row of slot p0
+    bool last_open;    // (warp-uniform) the chunk's last row may continue past s1
+};
+
+// targets of the lane's 8 slots (two 16-byte streaming loads when aligned and in range)
+__device__ __forceinline__ void blk_load(const int32_t* __restrict__ tgt, i64 s1, i64 sl, u32 (&t)[BLK_SPL]) {
+    if (sl + BLK_SPL <= s1 && ((reinterpret_cast<uintptr_t>(tgt) & 15) == 0)) {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4*>(tgt + sl));
+        const uint4 b = __ldcs(reinterpret_cast<const uint4*>(tgt + sl) + 1);
+        t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
+        t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < BLK_SPL; ++i) t[i] = sl + i < s1 ? (u32)__ldcs(tgt + sl + i) : 0u;
+    }
+}
+
+// the lane's 8 slot values, two 16-byte streaming stores when aligned and in range
+__device__ __forceinline__ void blk_store(u32* __restrict__ out, i64 s1, i64 sl, const u32 (&v)[BLK_SPL]) {
+    if (sl + BLK_SPL <= s1 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+        __stcs(reinterpret_cast<uint4*>(out + sl), make_uint4(v[0], v[1], v[2], v[3]));
+        __stcs(reinterpret_cast<uint4*>(out + sl) + 1, make_uint4(v[4], v[5], v[6], v[7]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < BLK_SPL; ++i)
+            if (sl + i < s1) __stcs(out + sl + i, v[i]);
+    }
+}
+
+// Row structure of chunk [s0, s1) whose first slot lies in row `base` (the nonempty row
+// containing s0).  All 32 lanes call it.
+__device__ __forceinline__ BlkRows blk_rows(const i64* __restrict__ off, i64 n, i64 s0, i64 s1, u32 base, int lane,
+                                            BlkSmem& sm) {
+    __syncwarp();   // the transposes' reads of xp (aliasing row) are done
+    if (lane < WCH / 32) sm.mask[lane] = 0u;
+    __syncwarp();
+    const i64 len = s1 - s0;
+    bool last_open = false;
+    for (i64 v0 = base;; v0 += 32) {
+        const i64 v = v0 + lane;
+        const i64 a = v < n ? off[v] : off[n];
+        i64 b = __shfl_down_sync(0xFFFFFFFFu, a, 1);
+        if (lane == 31) b = v + 1 <= n ? off[v + 1] : off[n];
+        const i64 p = a - s0;
+        if (b > a && p >= 0 && p < len) {          // a nonempty row starts inside the chunk
+            sm.row[p] = (u32)v;
+            atomicOr(&sm.mask[p >> 5], 1u << (p & 31));
+        }
+        // the chunk's last row: the nonempty row containing slot s1 - 1
+        const bool holds_last = b > a && a < s1 && b >= s1;
+        const unsigned hl = __ballot_sync(0xFFFFFFFFu, holds_last);
+        if (hl) last_open = __shfl_sync(0xFFFFFFFFu, b, __ffs(hl) - 1) > s1;
+        const i64 bl = __shfl_sync(0xFFFFFFFFu, b, 31);
+        if (bl >= s1 || v0 + 32 >= n) break;      // warp-uniform: no later row starts in the chunk
+    }
+    __syncwarp();
+    BlkRows r;
+    const int p0 = BLK_SPL * lane;
+    r.mb = (sm.mask[lane >> 2] >> (8 * (lane & 3))) & 0xFFu;
+    r.last_open = last_open;
+    // row of p0: the last start at or before p0, else base
+    u32 rf = base;
+    int wi = p0 >> 5;
+    u32 bits = sm.mask[wi] & (((p0 & 31) == 31) ? 0xFFFFFFFFu : ((2u << (p0 & 31)) - 1u));
+    while (!bits && wi > 0) bits = sm.mask[--wi];
+    if (bits) rf = sm.row[32 * wi + 31 - __clz(bits)];
+    r.r_first = rf;
+    return r;
+}
+
+// Segmented inclusive scan over lanes of (mn, mx) with head flags; `started` returns
+// whether the segment ending at this lane contains a head (began inside the chunk).
+__device__ __forceinline__ void blk_seg_scan(int lane, bool head, u32& mn, u32& mx, bool& started) {
+    bool f = head;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 a = __shfl_up_sync(0xFFFFFFFFu, mn, o);
+        const u32 b = __shfl_up_sync(0xFFFFFFFFu, mx, o);
+        const bool g = __shfl_up_sync(0xFFFFFFFFu, (int)f, o) != 0;
+        if (lane >= o && !f) {
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+            f = g;
+        }
+    }
+    started = f;
 }
 
 }  // namespace pg

@@ -1,6 +1,7 @@
 """CPU: lane-exact emulation of the warp-chunk slot->row resolution and row segmentation
 (paper_2404_17101_b200/csrc/wchunk.cuh), checked against brute force on the golden graphs
-plus CSRs dominated by empty rows (isolated vertices, as in RMAT).  Catches index
+plus CSRs dominated by empty rows (isolated vertices, as in RMAT), and of the blocked
+chunk protocol of k_tags_blk (row starts, sequential lane reduce, segmented scan, writes).  Catches index
 arithmetic bugs without a GPU; the GPU parity tests check the kernels themselves."""
 
 import numpy as np
@@ -105,13 +106,44 @@ def test_mostly_empty_rows():
             check_csr(off)
 
 
-def emulate_tags(off, vals, first):
-    """Lane-exact emulation of k_tags' segment reduce + carry/flush/atomic write protocol.
-    Returns W (min, max) per row; W starts at (first, first) like the preorder pass."""
+def blk_rows(off, n, s0, s1, base):
+    """Lane-exact emulation of wchunk.cuh blk_rows: per-lane start bytes, row of each
+    lane's first slot, the row id at every start, and whether the chunk's last row
+    continues past s1."""
+    mask, rowat, last_open = 0, {}, False
+    v0 = base
+    while True:
+        a = [int(off[v]) if v < n else int(off[n]) for v in range(v0, v0 + 32)]
+        b = [int(off[v + 1]) if v + 1 <= n else int(off[n]) for v in range(v0, v0 + 32)]
+        for lane in range(32):
+            p = a[lane] - s0
+            if b[lane] > a[lane] and 0 <= p < s1 - s0:
+                rowat[p] = v0 + lane
+                mask |= 1 << p
+        hl = [lane for lane in range(32) if b[lane] > a[lane] and a[lane] < s1 and b[lane] >= s1]
+        if hl:
+            last_open = b[hl[0]] > s1
+        if b[31] >= s1 or v0 + 32 >= n:
+            break
+        v0 += 32
+    mb, rfirst = [], []
+    for lane in range(32):
+        p0 = 8 * lane
+        mb.append((mask >> p0) & 0xFF)
+        below = mask & ((2 << p0) - 1)
+        rfirst.append(rowat[below.bit_length() - 1] if below else base)
+    return mb, rfirst, rowat, last_open
+
+
+def emulate_tags_blk(off, vals, first):
+    """Lane-exact emulation of k_tags_blk (sequential lane reduce, segmented warp scan,
+    boundary writes).  Returns W (min, max) per row; W starts at (first, first) like the
+    preorder pass."""
     n = off.shape[0] - 1
     m = int(off[-1])
+    INV = 0xFFFFFFFF
     W = [[int(first[r]), int(first[r])] for r in range(n)]
-    stores = {}                     # rows written without atomics (must be written once)
+    stores = {}
 
     def write(row, mn, mx, atomic):
         f = int(first[row])
@@ -125,62 +157,75 @@ def emulate_tags(off, vals, first):
 
     for c in range((m + WCH - 1) // WCH):
         s0, s1 = c * WCH, min(c * WCH + WCH, m)
-        cur = chunk_row(off, n, s0)
-        crw, cmn, cmx, cbefore = None, None, None, False
-        for k in range(8):
-            sb = s0 + 32 * k
-            if sb >= s1:
-                break
-            valid = [sb + lane < s1 for lane in range(32)]
-            rows = resolve(off, n, cur, sb, valid)
-            cur = rows[31]
-            segs = segments(rows, valid)
-            mn = [None] * 32
-            mx = [None] * 32
-            for lane in range(32):
-                if valid[lane]:
-                    lo, hi, _, _ = segs[lane]
-                    seg_vals = [vals[sb + i] for i in range(lo, hi + 1)]
-                    mn[lane], mx[lane] = min(seg_vals), max(seg_vals)
-            row0 = rows[0]
-            if crw is not None and crw != row0:
-                write(crw, cmn, cmx, cbefore)
-                crw = None
-            merged = crw is not None
-            before = [False] * 32
-            for lane in range(32):
-                lo = segs[lane][0]
-                if merged and lo == 0 and valid[lane]:
-                    mn[lane], mx[lane] = min(mn[lane], cmn), max(mx[lane], cmx)
-                before[lane] = lo == 0 and (cbefore if merged else k == 0)
-            has_next = sb + 32 < s1
-            for lane in range(32):
-                lo, hi, _, cut_right = segs[lane]
-                if valid[lane] and lane == lo and not (cut_right and has_next):
-                    write(rows[lane], mn[lane], mx[lane], before[lane] or cut_right)
-            if has_next:
-                crw, cmn, cmx, cbefore = rows[31], mn[31], mx[31], before[31]
+        mb, rfirst, rowat, last_open = blk_rows(off, n, s0, s1, chunk_row(off, n, s0))
+        T, H, R, head, hst, inner = [], [], [], [], [], []
+        for lane in range(32):
+            sl = s0 + 8 * lane
+            r, mn, mx, hmn, hmx, in_head = rfirst[lane], INV, 0, INV, 0, True
+            hstart = bool(mb[lane] & 1)
+            for i in range(8):
+                if i > 0 and (mb[lane] >> i) & 1:
+                    if in_head:
+                        hmn, hmx, in_head = mn, mx, False
+                        if hstart:
+                            write(r, mn, mx, False)
+                    else:
+                        write(r, mn, mx, False)
+                    r, mn, mx = rowat[8 * lane + i], INV, 0
+                if sl + i < s1:
+                    mn, mx = min(mn, int(vals[sl + i])), max(mx, int(vals[sl + i]))
+            T.append((mn, mx))
+            H.append((hmn, hmx))
+            R.append(r)
+            hst.append(hstart)
+            inner.append((mb[lane] & 0xFE) != 0)
+            head.append(hstart or inner[-1])
+        # segmented inclusive scan (sequential equivalent of blk_seg_scan)
+        C, started = [], []
+        for lane in range(32):
+            if head[lane] or lane == 0:
+                C.append(T[lane])
+                started.append(head[lane])
             else:
-                crw = None
+                C.append((min(C[-1][0], T[lane][0]), max(C[-1][1], T[lane][1])))
+                started.append(started[-1])
+        for lane in range(32):
+            if inner[lane] and not hst[lane]:
+                tmn, tmx = H[lane]
+                pst = False
+                if lane > 0:
+                    tmn, tmx = min(tmn, C[lane - 1][0]), max(tmx, C[lane - 1][1])
+                    pst = started[lane - 1]
+                write(rfirst[lane], tmn, tmx, not pst)
+            if lane < 31 and hst[lane + 1]:
+                write(R[lane], C[lane][0], C[lane][1], not started[lane])
+            if lane == 31:
+                write(R[lane], C[lane][0], C[lane][1], (not started[lane]) or last_open)
     return W
 
 
-def test_tags_write_protocol():
-    rng = np.random.default_rng(3)
-    for trial in range(25):
+def _random_csrs(seed, trials):
+    rng = np.random.default_rng(seed)
+    for trial in range(trials):
         n = int(rng.integers(20, 400))
         deg = np.where(rng.random(n) < 0.5, 0, rng.integers(1, 12, n))
         if trial % 3 == 0:
             deg[int(rng.integers(0, n))] = int(rng.integers(200, 900))   # hub spanning chunks
         if trial % 4 == 0:
             deg[rng.integers(0, n, 5)] = 32                              # exact window sizes
+        if trial % 5 == 0:
+            deg[rng.integers(0, n, 5)] = 8                               # exact lane sizes
+        if trial % 7 == 0:
+            deg[:] = np.where(rng.random(n) < 0.9, 0, 1)                 # mostly empty rows
         off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
-        m = int(off[-1])
-        if m == 0:
+        if off[-1] == 0:
             continue
-        vals = rng.integers(0, 10 * n, m)
-        first = rng.permutation(n)
-        W = emulate_tags(off, vals, first)
+        yield trial, n, off, rng.integers(0, 10 * n, int(off[-1])), rng.permutation(n)
+
+
+def test_tags_blk_write_protocol():
+    for trial, n, off, vals, first in _random_csrs(5, 60):
+        W = emulate_tags_blk(off, vals, first)
         for r in range(n):
             seg = vals[off[r]:off[r + 1]]
             want = [int(first[r]), int(first[r])] if seg.shape[0] == 0 else \
