@@ -18,7 +18,7 @@
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags_blk (per slot, blocked chunks), k_rmq_block/level/query (sparse table)
 //   S5 Last-CC    k_cc2_local / k_cc2_tree (non-fence tree edges, preorder blocks in shared
-//                 memory first), k_cc2_sample, k_giant, k_cc2_rest(+heavy)
+//                 memory first), k_cc2_xmax, k_giant, k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
 #include <cstdio>
@@ -847,24 +847,12 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 }
 
 // --------------------------------------------------------------------------
-// S5: Last-CC over cross edges.  Sampling first (Afforest): each vertex links NSAMPLE2
-// cross edge among the LAST SCAN2 slots of its row, so the big skeleton component forms
-// before the sampled-giant rows are skipped by the full pass.  The last slots hold the
-// largest neighbour ids; in a power-law graph the first ones are hubs, mostly ancestors
-// (tree/back edges), and sampling them fails to form the giant (sweep: 308 ms vs 136 ms).
+// S5: Last-CC over cross edges.  Sampling first (Afforest): every position links the cross
+// edge its high tag points at (k_cc2_xmax), so the big skeleton component forms before
+// the sampled-giant rows are skipped by the full pass.  It replaced sampling the last two
+// slots of each row (two random (first, last) gathers per vertex): C5a Last-CC 18.2 ->
+// 12.8 ms, C4 4.4 -> 3.2, C3 1.6 -> 1.4, C2 0.81 -> 0.48.
 // --------------------------------------------------------------------------
-#ifndef PG_NSAMPLE2
-#define PG_NSAMPLE2 1
-#endif
-#ifndef PG_SCAN2
-#define PG_SCAN2 2
-#endif
-#ifndef PG_SAMPLE2_MODE
-#define PG_SAMPLE2_MODE 1
-#endif
-constexpr int NSAMPLE2 = PG_NSAMPLE2;
-constexpr int SCAN2 = PG_SCAN2;
-
 __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
     return !((fu.x <= fw.x && fw.x <= fu.y) || (fw.x <= fu.x && fu.x <= fw.y));
 }
@@ -898,36 +886,16 @@ __global__ void k_cc2_tree(i64 n, const u32* __restrict__ FPF, u32* C) {
     if ((f >> LOCAL_LB) != (u32)(i >> LOCAL_LB)) uf_link(C, (u32)i, f);
 }
 
-__global__ void k_cc2_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt,
-                             const uint2* __restrict__ FL, u32* C) {
-    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
-    i64 a = off[u], b = off[u + 1];
-    if (b - a < 2) return;     // a degree-1 vertex has only its tree edge
-    const i64 deg = b - a;
-    const int cnt = (int)(deg < SCAN2 ? deg : SCAN2);
-    uint2 fu = FL[u];
-    uint2 fw[SCAN2];           // all loads issued before the first test
-#pragma unroll
-    for (int k = 0; k < SCAN2; ++k) {
-        // which slots: PG_SAMPLE2_MODE 0 = first, 1 = last, 2 = spread over the row
-#if PG_SAMPLE2_MODE == 1
-        const i64 s = b - 1 - k;
-#elif PG_SAMPLE2_MODE == 2
-        const i64 s = a + (deg * k) / SCAN2;
-#else
-        const i64 s = a + k;
-#endif
-        fw[k] = k < cnt ? FL[(u32)tgt[s]] : fu;
-    }
-    int linked = 0;
-#pragma unroll
-    for (int k = 0; k < SCAN2; ++k) {
-        if (linked < NSAMPLE2 && k < cnt && is_cross(fu, fw[k])) {
-            uf_link(C, fu.x, fw[k].x);
-            ++linked;
-        }
-    }
+// Sampling without gathers: the high tag w2[i] (before the RMQ) is the
+// largest preorder rank among the neighbours of the vertex at position i.  When it lies
+// beyond the vertex's subtree (w2 > last) that neighbour is neither a descendant nor an
+// ancestor, so the edge is a cross edge of the skeleton: link it.  One coalesced read of W
+// and E per position replaces two random (first, last) gathers per vertex.
+__global__ void k_cc2_xmax(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E, u32* C) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u32 hi = __ldcs(&W[i].y);
+    if (hi > __ldcs(E + i)) uf_link(C, (u32)i, hi);
 }
 
 // over preorder positions i (vertex PV[i]); tree roots have only back edges (every vertex
@@ -1485,7 +1453,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // ---- S5 Last-CC over cross edges
     PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.C));
     PG_K(k_cc2_tree<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.C));
-    PG_K(k_cc2_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.C));
+    PG_K(k_cc2_xmax<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.C));
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
