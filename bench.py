@@ -142,6 +142,25 @@ def traffic_from_profiles(config, kernel):
         return None
 
 
+def random_access_roofline(traffic, kernel_ms):
+    """The dominant kernels are random-gather bound, and on this part every HBM miss moves
+    a whole 128-byte line, so their ceiling is lines/s, not bytes/s: DRAM lines fetched per
+    launch (ncu traffic / 128) over the live kernel time, against the measured random-line
+    rate of tools/probes/gather_probe.cu (profiles/random_access_peak.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "random_access_peak.json")) as f:
+            pk = json.load(f)
+    except Exception:
+        return None
+    if not traffic:
+        return None
+    lines = traffic / pk["bytes_per_miss"]
+    ach = lines / (kernel_ms / 1e3)
+    return {"achieved_lines_per_s": ach, "peak_lines_per_s": pk["hbm_random_lines_per_s"],
+            "frac": ach / pk["hbm_random_lines_per_s"], "lines_per_launch": lines,
+            "peak_source": "profiles/random_access_peak.json (measured, tools/probes/gather_probe.cu)"}
+
+
 # --------------------------------------------------------------------------------------
 # reference arm: the reference's CPU BCC (Hopcroft-Tarjan, oracles.py:119-201) restated in
 # C (oracle/), on all host cores, on a bounded sample of the same workload
@@ -314,7 +333,8 @@ def run_ours(args, rank, world, local):
     traffic = traffic_from_profiles(args.config, KERNEL_NAMES[dom])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": KERNEL_NAMES[dom],
-                "algorithmic_bytes_per_launch": kb, "kernel_ms": stage_ms[dom], "peak_source": peak_src}
+                "algorithmic_bytes_per_launch": kb, "kernel_ms": stage_ms[dom], "peak_source": peak_src,
+                "random_access": random_access_roofline(traffic, stage_ms[dom])}
     pipeline = {"algorithmic_bytes": pipe_bytes, "model": "56*M + 180*n (SURVEY 8(d))",
                 "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
                 "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
