@@ -11,7 +11,7 @@
 //     (a fence child can share p's skeleton component through a cross edge).
 //
 // Stages (kernels), all stream-ordered, no host synchronisation:
-//   S2 First-CC   k_init, k_chunk_rows, k_cc_local (shared-memory union-find per id block),
+//   S2 First-CC   k_chunk_rows, k_cc_local (shared-memory union-find per id block),
 //                 k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
 //   S3 rooting    k_arc_link, k_arc_close (root chain, isolated slots), ruling-set list ranking (k_lr_walk1,
@@ -149,14 +149,6 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
 // S2: First-CC (spanning forest by union-find with hook capture; Afforest-style
 // neighbour sampling, then skip the sampled giant component)
 // --------------------------------------------------------------------------
-__global__ void k_init(i64 n, u32* P, uint2* HAB, u32* HEAD, u32* C) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    P[v] = (u32)v;
-    C[v] = (u32)v;
-    reinterpret_cast<uint4*>(HAB)[v] = make_uint4(PG_INV, PG_INV, 0u, 0u);   // whole 16-byte record
-    HEAD[v] = PG_INV;
-}
 
 __global__ void k_canon_init(i64 n, u32* UCNT, i64 nlab, u32* CANON) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -196,12 +188,19 @@ __device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
     return PG_INV;
 }
 
+// It also initialises its block's hook records and out-arc heads (no separate init pass;
+// P is published for every id below, and Last-CC's C by k_cc2_local).
 __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restrict__ off,
-                                                      const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
+                                                      const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                                                      u32* HEAD) {
     __shared__ u32 sp[LOCAL_B];
     const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
     const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
-    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) sp[i] = (u32)i;
+    for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
+        sp[i] = (u32)i;
+        reinterpret_cast<uint4*>(HAB)[b0 + i] = make_uint4(PG_INV, PG_INV, 0u, 0u);   // whole 16-byte record
+        HEAD[b0 + i] = PG_INV;
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
         i64 v = b0 + i, a = off[v], b = off[v + 1];
@@ -1403,9 +1402,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    PG_K(k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C));
     if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
@@ -1519,8 +1517,7 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     const int B = 256;
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     if (n > 0) {
-        k_init<<<nblk(n, B), B, 0, st>>>(n, w.P, w.HAB, w.HEAD, w.C);
-        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB);
+        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD);
         k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB);
         k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
