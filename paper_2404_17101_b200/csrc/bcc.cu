@@ -38,14 +38,23 @@ constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual 
 #ifndef PG_NSAMPLE
 #define PG_NSAMPLE 2
 #endif
-#ifndef PG_LR_K
-#define PG_LR_K 64
-#endif
 #ifndef PG_LOCAL_LB
 #define PG_LOCAL_LB 13
 #endif
 constexpr int NSAMPLE = PG_NSAMPLE;    // neighbours linked per vertex before giant detection
-constexpr u32 LR_K = PG_LR_K;          // list-ranking ruler spacing (power of two)
+// List-ranking ruler spacing 2^lr_shift(n): long walks amortise the pointer jumping on big
+// tours, but a walk is a chain of dependent loads, so small graphs (L2-resident, launch-
+// and latency-bound) use short ones.  PASGAL_BCC_LR_SHIFT overrides it (sweeps).
+static inline int lr_shift(i64 n) {
+    const char* e = getenv("PASGAL_BCC_LR_SHIFT");
+    const int v = e ? atoi(e) : 0;
+    if (v >= 1 && v <= 10) return v;
+    // measured (profiles/r01_sweeps.txt): C1 2^16 -> 3, C2 2^20 and C3 2^24 -> 4,
+    // C4 2^25 -> 5-6, C5a 2^28 -> 6-7
+    if (n < ((i64)1 << 18)) return 3;
+    if (n < ((i64)1 << 25)) return 4;
+    return n < ((i64)1 << 28) ? 6 : 7;
+}
 constexpr int GIANT_SAMPLES = 1024;
 constexpr int HEAVY_GRID = 148 * 4;
 
@@ -88,6 +97,7 @@ struct Ws {
     u64* SCAN;
     Ctr* ctr;
     i64 nb, lv, ns, nch;
+    u32 lrs;      // list-ranking ruler spacing = 1 << lrs
 };
 
 static inline i64 rmq_levels(i64 nb) {
@@ -108,7 +118,8 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     i64 L = 2 * nn;
     w.nb = cdiv(nn, 32);
     w.lv = rmq_levels(w.nb);
-    w.ns = cdiv(L, LR_K) + 1;   // + the head ruler
+    w.lrs = (u32)lr_shift(n);
+    w.ns = cdiv(L, (i64)1 << w.lrs) + 1;   // + the head ruler
     w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
@@ -484,7 +495,7 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restri
 }
 
 // ruling-set list ranking over succ(a) = NEXT[a^1].  Rulers: every on-tour arc a with
-// a % LR_K == 0, plus the head (ruler index nsk).  walk1: each ruler's sublist length and
+// a % 2^lrs == 0, plus the head (ruler index nsk).  walk1: each ruler's sublist length and
 // next ruler; Wyllie on the rulers; walk2: final positions (into HAB[2y+1]) and TA[position] = arc.
 struct TourInfo {
     u32 head;     // first arc of the list, PG_INV if the tour is empty
@@ -497,17 +508,17 @@ __device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, i64 n) {
     return t;
 }
 __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, const uint2* HAB, const u32* HEAD,
-                                            u32& x) {
+                                            u32 lrs, u32& x) {
     if (s < nsk) {
-        x = (u32)s * LR_K;
+        x = (u32)s << lrs;
         u32 v = x >> 1;
         return !(HAB[2 * (i64)v].x == PG_INV && HEAD[v] == PG_INV);   // isolated vertices are off the tour
     }
     x = t.head;
-    return t.head != PG_INV && (t.head & (LR_K - 1)) != 0;
+    return t.head != PG_INV && (t.head & ((1u << lrs) - 1u)) != 0;
 }
 
-__global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
+__global__ void k_lr_walk1(i64 n, i64 ns, u32 lrs, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
                            const u32* __restrict__ HEAD, const Ctr* ctr, u32* SPLEN,
                            u32* SPNEXT) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -515,7 +526,7 @@ __global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
     const TourInfo t = tour_info(ctr, n);
     const i64 nsk = ns - 1;
     u32 x;
-    if (!ruler_start(s, nsk, t, HAB, HEAD, x)) {
+    if (!ruler_start(s, nsk, t, HAB, HEAD, lrs, x)) {
         SPLEN[s] = 0;
         SPNEXT[s] = PG_INV;
         return;
@@ -524,9 +535,9 @@ __global__ void k_lr_walk1(i64 n, i64 ns, const u32* __restrict__ NEXT, const ui
     do {
         ++cnt;
         x = __ldg(NEXT + (x ^ 1u));
-    } while (x != PG_INV && (x & (LR_K - 1)) != 0);   // the head is never revisited
+    } while (x != PG_INV && (x & ((1u << lrs) - 1u)) != 0);   // the head is never revisited
     SPLEN[s] = cnt;
-    SPNEXT[s] = x == PG_INV ? PG_INV : x / LR_K;
+    SPNEXT[s] = x == PG_INV ? PG_INV : x >> lrs;
 }
 
 // Wyllie pointer jumping on the rulers: suffix sums of sublist lengths
@@ -546,7 +557,7 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
 
 constexpr int LR_T = 256;
 
-__global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, const u32* __restrict__ NEXT,
+__global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, u32 lrs, const u32* __restrict__ NEXT,
                                                    const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
                                                    const Ctr* ctr, const u32* __restrict__ SUFFIX, uint2* HABW,
                                                    u32* TA) {
@@ -555,7 +566,7 @@ __global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, const u32* __r
     if (s >= ns) return;
     const TourInfo t = tour_info(ctr, n);
     u32 x;
-    if (!ruler_start(s, ns - 1, t, HAB, HEAD, x)) return;
+    if (!ruler_start(s, ns - 1, t, HAB, HEAD, lrs, x)) return;
     const u32 pos0 = t.len - SUFFIX[s];
     u32 pos = pos0;
     // TA[pos] = arc, staged per thread so that whole 32-byte sectors (8 positions, aligned)
@@ -578,7 +589,7 @@ __global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, const u32* __r
         }
         ++pos;
         x = nx;
-    } while (x != PG_INV && (x & (LR_K - 1)) != 0);
+    } while (x != PG_INV && (x & ((1u << lrs) - 1u)) != 0);
     // the unfinished last sector (possibly also the first): positions [max(pos & ~7, pos0), pos)
     for (u32 q = (pos & ~7u) > pos0 ? (pos & ~7u) : pos0; q < pos; ++q) TA[q] = buf[q & 7u];
 }
@@ -1420,14 +1431,14 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
-    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[0],
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[0],
                                                      w.SPNEXT[0]));
     int cur = 0;
     for (i64 span = 1; span < w.ns; span <<= 1) {
         PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
         cur ^= 1;
     }
-    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[cur],
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[cur],
                                                      w.HAB, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));

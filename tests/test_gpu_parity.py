@@ -361,3 +361,17 @@ def test_canonical_checksum_device_equals_host():
     ref = oracle.bcc_hopcroft_tarjan(g.offsets, g.targets)
     assert pg.canonical_checksum_device(r.edge_label, r.artic_bits, r.bcc_count) == pg.canonical_checksum(
         oracle.canonical_min_eid(g.offsets, g.targets, ref.edge_label), ref.articulation, ref.bcc_count)
+
+
+def test_ruler_spacings(monkeypatch):
+    """The list ranking's ruler spacing depends on n (2^3 for small graphs ... 2^7 at
+    2^28 vertices); every spacing must give the same output, on a power-law graph and on a
+    long path (one tour spanning many rulers)."""
+    dg = pg.gen_rmat(16, 8 << 16, seed=4)
+    n = 50_000
+    s = np.arange(n - 1)
+    chain = pg.symmetrize_edges(n, s, s + 1)
+    for shift in ["2", "5", "7", "9"]:
+        monkeypatch.setenv("PASGAL_BCC_LR_SHIFT", shift)
+        _parity_device_graph(dg)
+        assert _parity_device_graph(chain) == n - 1
