@@ -179,10 +179,11 @@ __device__ __forceinline__ void blk_store(u32* __restrict__ out, i64 s1, i64 sl,
     }
 }
 
-// Row structure of chunk [s0, s1) whose first slot lies in row `base` (the nonempty row
-// containing s0).  All 32 lanes call it.
-__device__ __forceinline__ BlkRows blk_rows(const i64* __restrict__ off, i64 n, i64 s0, i64 s1, u32 base, int lane,
-                                            BlkSmem& sm) {
+// Row starts of chunk [s0, s1) whose first slot lies in row `base` (the nonempty row
+// containing s0): the mask and the row id at each start, in sm.  Returns whether the
+// chunk's last row continues past s1.  All 32 lanes call it.
+__device__ __forceinline__ bool blk_scan_rows(const i64* __restrict__ off, i64 n, i64 s0, i64 s1, u32 base, int lane,
+                                              BlkSmem& sm) {
     __syncwarp();   // the transposes' reads of xp (aliasing row) are done
     if (lane < WCH / 32) sm.mask[lane] = 0u;
     __syncwarp();
@@ -206,6 +207,13 @@ __device__ __forceinline__ BlkRows blk_rows(const i64* __restrict__ off, i64 n, 
         if (bl >= s1 || v0 + 32 >= n) break;      // warp-uniform: no later row starts in the chunk
     }
     __syncwarp();
+    return last_open;
+}
+
+// The blocked view: per lane its start byte and the row of its first slot.
+__device__ __forceinline__ BlkRows blk_rows(const i64* __restrict__ off, i64 n, i64 s0, i64 s1, u32 base, int lane,
+                                            BlkSmem& sm) {
+    const bool last_open = blk_scan_rows(off, n, s0, s1, base, lane, sm);
     BlkRows r;
     const int p0 = BLK_SPL * lane;
     r.mb = (sm.mask[lane >> 2] >> (8 * (lane & 3))) & 0xFFu;
