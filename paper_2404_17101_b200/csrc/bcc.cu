@@ -702,11 +702,14 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
     const i64 sl = s0 + BLK_SPL * lane;
     u32 fw[BLK_SPL];
     {
+        // FIRST lines are kept in L2 ahead of the W stores and offsets (evict_last): C5a
+        // tags 36.8 -> 36.3 ms
+        const u64 pol = policy_evict_last();
         u32 g[WCH_U];   // strided: one gather instruction covers 32 consecutive slots
         wc_load(tgt, m, c, lane, g);
 #pragma unroll
         for (int k = 0; k < WCH_U; ++k)
-            if (s0 + 32 * k + lane < s1) g[k] = __ldg(FIRST + g[k]);
+            if (s0 + 32 * k + lane < s1) g[k] = ld_keep(FIRST + g[k], pol);
         blk_transpose(sm, lane, g, fw);
     }
     const BlkRows br = blk_rows(off, n, s0, s1, crow[c], lane, sm);

@@ -28,6 +28,17 @@ __host__ __device__ __forceinline__ u64 draw(u64 seed, u64 ctr) { return sm64(sm
 // same kernel; L1 is not coherent, so parent reads bypass it (ld.global.cg).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ u32 ldcg(const u32* p) { return __ldcg(p); }
+// L2 evict_last access policy and a read-only load under it
+__device__ __forceinline__ u64 policy_evict_last() {
+    u64 pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ u32 ld_keep(const u32* p, u64 pol) {
+    u32 r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
 __device__ __forceinline__ void stcg(u32* p, u32 v) { __stcg(p, v); }
 
 __device__ __forceinline__ u64 ld_volatile_u64(const u64* p) {
