@@ -17,8 +17,9 @@
 //   S3 rooting    k_arc_link, k_arc_close (root chain, isolated slots), ruling-set list ranking (k_lr_walk1,
 //                 k_wyllie, k_lr_walk2), preorder scan (first/last/parent)   Euler tour
 //   S4 tags       k_tags_blk (per slot, blocked chunks), k_rmq_block/level/query (sparse table)
-//   S5 Last-CC    k_cc2_local / k_cc2_tree (non-fence tree edges, preorder blocks in shared
-//                 memory first), k_cc2_xmax, k_giant, k_cc2_rest(+heavy)
+//   S5 Last-CC    k_cc2_local (non-fence tree edges and high-tag cross edges inside preorder
+//                 blocks, shared memory), k_cc2_links (the block-crossing ones), k_giant,
+//                 k_cc2_rest(+heavy)
 //   S6 labels     k_compress_final, k_artic, k_labels, k_finish
 //   canonical     k_canon_count, scan, k_canon_min, k_canon_apply     (flag CANONICAL)
 #include <cstdio>
@@ -861,7 +862,7 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
 
 // --------------------------------------------------------------------------
 // S5: Last-CC over cross edges.  Sampling first (Afforest): every position links the cross
-// edge its high tag points at (k_cc2_xmax), so the big skeleton component forms before
+// edge its high tag points at (k_cc2_local / k_cc2_links), so the big skeleton component forms before
 // the sampled-giant rows are skipped by the full pass.  It replaced sampling the last two
 // slots of each row (two random (first, last) gathers per vertex): C5a Last-CC 18.2 ->
 // 12.8 ms, C4 4.4 -> 3.2, C3 1.6 -> 1.4, C2 0.81 -> 0.48.
@@ -875,7 +876,8 @@ __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
 // Last-CC local phase over preorder positions: non-fence tree edges (i, parent position)
 // inside a block of LOCAL_B positions are joined in shared memory (a child's parent is
 // usually a few positions back), then C[i] = block root is published.
-__global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restrict__ FPF, u32* C) {
+__global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restrict__ FPF, const uint2* __restrict__ W,
+                                                       const u32* __restrict__ E, u32* C) {
     __shared__ u32 sp[LOCAL_B];
     const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
     const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
@@ -883,6 +885,10 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restr
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
         u32 f = FPF[b0 + i];
+        {     // the high tag's cross edge (k_cc2_links), when it stays in the block
+            const u32 hi = __ldcs(&W[b0 + i].y);
+            if (hi > __ldcs(E + b0 + i) && (i64)hi < b0 + LOCAL_B) slink(sp, (u32)i, (u32)(hi - b0));
+        }
         if (f & 0x80000000u) continue;     // fence, or a root (PG_INV)
         if ((i64)f >= b0) slink(sp, (u32)i, (u32)(f - b0));
     }
@@ -890,25 +896,26 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restr
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) C[b0 + i] = (u32)b0 + sfind(sp, (u32)i);
 }
 
-// non-fence tree edges whose parent lies in an earlier block
-__global__ void k_cc2_tree(i64 n, const u32* __restrict__ FPF, u32* C) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    u32 f = FPF[i];
-    if (f & 0x80000000u) return;
-    if ((f >> LOCAL_LB) != (u32)(i >> LOCAL_LB)) uf_link(C, (u32)i, f);
-}
-
 // Sampling without gathers: the high tag w2[i] (before the RMQ) is the
 // largest preorder rank among the neighbours of the vertex at position i.  When it lies
 // beyond the vertex's subtree (w2 > last) that neighbour is neither a descendant nor an
 // ancestor, so the edge is a cross edge of the skeleton: link it.  One coalesced read of W
 // and E per position replaces two random (first, last) gathers per vertex.
-__global__ void k_cc2_xmax(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E, u32* C) {
+//
+// Both block-crossing global links of a position in one pass: its non-fence tree edge and
+// the cross edge of its high tag (a cross edge never points into its own subtree, so
+// hi > last >= i and a block-local one was taken by k_cc2_local).
+__global__ void k_cc2_links(i64 n, const u32* __restrict__ FPF, const uint2* __restrict__ W,
+                            const u32* __restrict__ E, u32* C) {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const u32 f = FPF[i];
     const u32 hi = __ldcs(&W[i].y);
-    if (hi > __ldcs(E + i)) uf_link(C, (u32)i, hi);
+    const u32 e = __ldcs(E + i);
+    const bool tree = !(f & 0x80000000u) && (f >> LOCAL_LB) != (u32)(i >> LOCAL_LB);
+    const bool cross = hi > e && (hi >> LOCAL_LB) != (u32)(i >> LOCAL_LB);
+    if (tree) uf_link(C, (u32)i, f);
+    if (cross) uf_link(C, (u32)i, hi);
 }
 
 // over preorder positions i (vertex PV[i]); tree roots have only back edges (every vertex
@@ -1463,9 +1470,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
-    PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.C));
-    PG_K(k_cc2_tree<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.C));
-    PG_K(k_cc2_xmax<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.C));
+    PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
+    PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
