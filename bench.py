@@ -68,6 +68,44 @@ def reduce_over_ranks(total_ms, edges, device):
     return float(t.item()), float(e.item())
 
 
+def _sync():
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+
+
+def _allreduce(vals, op, device):
+    """Element-wise all-reduce of a list of floats (identity on one rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(v) for v in vals]
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=op)
+    return [float(v) for v in t.tolist()]
+
+
+def e2e_ranks(n, m, world, device):
+    """How many ranks run the e2e legs at once: each needs its pinned host CSR and pinned
+    output buffers (C5a: 19.2 + 17.3 GB), and N ranks on one node must not exhaust its
+    memory.  Ranks 0..k-1 run them concurrently, the rest wait at the same barriers; k is
+    the minimum over ranks so every rank takes the same decision."""
+    import torch.distributed as dist
+
+    need = (8 * (n + 1) + 4 * m) + (4 * m + n + 8)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    try:
+        import psutil
+
+        k = int(0.7 * psutil.virtual_memory().available // max(need, 1))
+    except Exception:
+        k = local_world
+    k = max(0, min(k, local_world)) * max(1, world // max(local_world, 1))
+    return int(_allreduce([k], dist.ReduceOp.MIN, device)[0]) if world > 1 else min(k, 1)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -343,15 +381,21 @@ def run_ours(args, rank, world, local):
     # ---- e2e through the public drop-in call with host buffers (pinned), H2D + D2H timed
     e2e = None
     if not args.no_e2e:
-        # host copy of the CSR (pinned), then free every device buffer of the device-timed
-        # arm: the e2e arms allocate their own (the pipelined one keeps two graphs in flight)
-        off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
-        tgt_h = torch.empty(m, dtype=torch.int32, pin_memory=True)
-        off_h.copy_(dg.offsets)
-        tgt_h.copy_(dg.targets)
-        del dg, ws, out, r
-        torch.cuda.empty_cache()
-        e2e = run_e2e(args, off_h, tgt_h, dev, n, m)
+        k = e2e_ranks(n, m, world, dev)
+        if k == 0:
+            e2e = {"unavailable": "host memory cannot hold one rank's pinned CSR and output buffers"}
+        else:
+            # host copy of the CSR (pinned), then free every device buffer of the device-timed
+            # arm: the e2e arms allocate their own (the pipelined one keeps two graphs in flight)
+            off_h = tgt_h = None
+            if rank < k:
+                off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+                tgt_h = torch.empty(m, dtype=torch.int32, pin_memory=True)
+                off_h.copy_(dg.offsets)
+                tgt_h.copy_(dg.targets)
+            del dg, ws, out, r
+            torch.cuda.empty_cache()
+            e2e = run_e2e(args, off_h, tgt_h, dev, n, m, rank < k, k, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -514,76 +558,107 @@ def verify_instances(graphs, sums):
             "checker": "oracle/bcc_oracle.c (C restatement of bcc_hopcroft_tarjan) + canonical_min_eid"}
 
 
-def run_e2e(args, off_h, tgt_h, dev, n, m):
+def run_e2e(args, off_h, tgt_h, dev, n, m, participate=True, k=1, world=1):
     """The same metric through pg.bcc(g): H2D of the CSR from pinned host memory, device
     validation (the reference's is_symmetric), FAST-BCC, D2H of labels + articulation bytes
     + count into pinned host buffers -- all inside the timed region, one call at a time.
     Also reported (not the headline): the same steps through pg.BccPipeline, which overlaps
-    one graph's H2D with the previous graph's D2H and BCC."""
+    one graph's H2D with the previous graph's D2H and BCC.
+    With N ranks, ranks 0..k-1 (k from e2e_ranks) run each leg concurrently between
+    barriers; the value is their summed edges over the slowest participant's time."""
     import torch
+    import torch.distributed as dist
 
     import paper_2404_17101_b200 as pg
 
-    g = pg.Graph(off_h.numpy(), tgt_h.numpy())
-    hb = pg.HostBuffers.allocate(n, m)
     steps = max(1, min(args.steps, args.e2e_steps))
-    res = pg.bcc(g, device=dev, host_out=hb)         # warm-up
-    torch.cuda.synchronize()
-    # split-out components (diagnostic only): H2D copy and device validation alone
-    t0 = time.perf_counter()
-    off_d = off_h.to(dev, non_blocking=True)
-    tgt_d = tgt_h.to(dev, non_blocking=True)
-    torch.cuda.synchronize()
-    h2d_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    pg.validate_device(off_d, tgt_d)
-    val_s = time.perf_counter() - t0
-    del off_d, tgt_d
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        res = pg.bcc(g, device=dev, host_out=hb)
-    dt = (time.perf_counter() - t0) / steps
     h2d = 8 * (n + 1) + 4 * m
     d2h = 4 * m + n + 8
-    del res, hb
-    out = {"value": (m // 2) / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    dt = h2d_s = val_s = 0.0
+    if participate:
+        g = pg.Graph(off_h.numpy(), tgt_h.numpy())
+        hb = pg.HostBuffers.allocate(n, m)
+        res = pg.bcc(g, device=dev, host_out=hb)         # warm-up
+        torch.cuda.synchronize()
+        # split-out components (diagnostic only): H2D copy and device validation alone
+        t0 = time.perf_counter()
+        off_d = off_h.to(dev, non_blocking=True)
+        tgt_d = tgt_h.to(dev, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pg.validate_device(off_d, tgt_d)
+        val_s = time.perf_counter() - t0
+        del off_d, tgt_d
+    _sync()
+    if participate:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = pg.bcc(g, device=dev, host_out=hb)
+        dt = (time.perf_counter() - t0) / steps
+        del res, hb
+    _sync()
+    edges, = _allreduce([(m // 2) if participate else 0], dist.ReduceOp.SUM, dev) if world > 1 else [m // 2]
+    dt, = _allreduce([dt], dist.ReduceOp.MAX, dev) if world > 1 else [dt]
+    out = {"value": edges / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": dt * 1e3, "steps": steps,
            "h2d_ms": round(h2d_s * 1e3, 1), "validate_ms": round(val_s * 1e3, 1),
            "path": "paper_2404_17101_b200.bcc(g) with host numpy CSR (pinned) -> H2D, validate, FAST-BCC, "
                    "D2H labels+articulation bytes+count (pinned)"}
+    if world > 1:
+        out["ranks"] = k
+        out["bytes_per_step_note"] = "h2d/d2h bytes are per participating rank"
     # pipelined: the same per-step copies and work, consecutive steps overlapped
     pg.release_workspace()
     torch.cuda.empty_cache()
     need = 2 * (4 * m + n + 8)                          # two pinned output slots per rank
-    world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
     try:
         import psutil
 
         avail = psutil.virtual_memory().available
     except Exception:
         avail = None
-    if avail is not None and avail < 1.5 * world * need:
-        out["pipelined"] = {"unavailable": f"host memory: {world} ranks x {need / 1e9:.1f} GB of pinned output "
-                                           f"slots exceed 2/3 of the {avail / 1e9:.0f} GB available"}
+    ok = avail is None or avail >= 1.5 * k * need      # k participants on this node
+    if world > 1:
+        ok = _allreduce([1.0 if ok else 0.0], dist.ReduceOp.MIN, dev)[0] > 0
+    if not ok:
+        out["pipelined"] = {"unavailable": f"host memory: {k} ranks x {need / 1e9:.1f} GB of pinned output "
+                                           f"slots exceed 2/3 of the {(avail or 0) / 1e9:.0f} GB available"}
         return out
-    try:
-        psteps = max(6, steps + 1)
-        pipe = pg.BccPipeline(device=dev)
-        for _ in pipe.run([g, g]):                     # warm-up: rings and workspaces
-            pass
-        torch.cuda.synchronize()
+    psteps = max(6, steps + 1)
+    pdt, oom = 0.0, 0.0
+    pipe = None
+    if participate:
+        try:
+            pipe = pg.BccPipeline(device=dev)
+            for _ in pipe.run([g, g]):                     # warm-up: rings and workspaces
+                pass
+            torch.cuda.synchronize()
+        except torch.cuda.OutOfMemoryError:
+            oom, pipe = 1.0, None
+    if world > 1:
+        oom = _allreduce([oom], dist.ReduceOp.MAX, dev)[0]
+    if oom:
+        del pipe
+        pg.release_workspace()
+        torch.cuda.empty_cache()
+        out["pipelined"] = {"unavailable": "out of device memory for two graphs in flight"}
+        return out
+    _sync()
+    if participate:
         t0 = time.perf_counter()
         for _ in pipe.run([g] * psteps):
             pass
         pdt = (time.perf_counter() - t0) / psteps
-        out["pipelined"] = {"value": (m // 2) / pdt, "unit": UNIT, "ms_per_step": pdt * 1e3, "steps": psteps,
-                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                            "path": "paper_2404_17101_b200.BccPipeline.run(graphs): H2D of step i+1 overlaps "
-                                    "BCC + D2H of step i (two-slot device rings, three streams); "
-                                    "fill and drain included"}
-        del pipe
-    except torch.cuda.OutOfMemoryError as e:
-        out["pipelined"] = {"unavailable": f"out of device memory for two graphs in flight: {str(e)[:80]}"}
+    _sync()
+    if world > 1:
+        pdt = _allreduce([pdt], dist.ReduceOp.MAX, dev)[0]
+    out["pipelined"] = {"value": edges / pdt, "unit": UNIT, "ms_per_step": pdt * 1e3, "steps": psteps,
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "path": "paper_2404_17101_b200.BccPipeline.run(graphs): H2D of step i+1 overlaps "
+                                "BCC + D2H of step i (two-slot device rings, three streams); "
+                                "fill and drain included"}
+    del pipe
     pg.release_workspace()
     torch.cuda.empty_cache()
     return out

@@ -56,3 +56,37 @@ def test_single_process_passthrough():
 
     assert bench.reduce_over_ranks(7.5, 42, "cpu") == (7.5, 42.0)
     assert bench.assign_instances(5, 0, 1) == [0, 1, 2, 3, 4]
+
+
+def _e2e_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+
+    small = bench.e2e_ranks(1000, 10000, world, "cpu")            # fits: every rank runs the e2e legs
+    huge = bench.e2e_ranks(1 << 40, 1 << 44, world, "cpu")        # does not fit anywhere
+    mx = bench._allreduce([rank + 1.0, -rank], dist.ReduceOp.MAX, "cpu")
+    q.put((rank, small, huge, mx))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_e2e_participants_agree_across_ranks():
+    """bench.py's e2e legs at N ranks: the number of concurrently participating ranks is
+    bounded by host memory (pinned CSR + outputs per rank) and identical on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_e2e_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+    assert [r[1] for r in res] == [2, 2]
+    assert [r[2] for r in res] == [0, 0]
+    assert res[0][3] == res[1][3] == [2.0, 0.0]
