@@ -375,3 +375,34 @@ def test_ruler_spacings(monkeypatch):
         monkeypatch.setenv("PASGAL_BCC_LR_SHIFT", shift)
         _parity_device_graph(dg)
         assert _parity_device_graph(chain) == n - 1
+
+
+@pytest.mark.slow
+def test_config_c5a_full_size_against_pinned_oracle_hashes():
+    """C5a (RMAT 2^28, 4.26e9 slots) at full size: canonical labels, articulation bitmap and
+    bcc_count hash-equal to the C oracle's on the same CSR (a 43-minute oracle run whose
+    hashes are committed in tests/golden/c5a_oracle_hashes.json), for two sampling seeds."""
+    import hashlib
+    import json
+    import os
+
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("C5a needs a 180 GB B200")
+    want = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c5a_oracle_hashes.json")))
+
+    def h(a):
+        return hashlib.blake2b(np.ascontiguousarray(a).view(np.uint8), digest_size=16).hexdigest()
+
+    dg = pg.make_config("c5a")
+    assert (dg.n, dg.m) == (want["n"], want["m_slots"])
+    for seed in (0, 7):
+        r = pg.bcc_device(dg.offsets, dg.targets, seed=seed, canonical=True, validate=True)
+        lab, art, cnt = _host_out(r, dg.n)
+        del r
+        assert cnt == want["count"], seed
+        assert h(art) == want["artic"], seed
+        assert h(lab) == want["labels"], seed
+        del lab, art
+    del dg
+    pg.release_workspace()
+    torch.cuda.empty_cache()
