@@ -11,7 +11,7 @@
 //     (a fence child can share p's skeleton component through a cross edge).
 //
 // Stages (kernels), all stream-ordered, no host synchronisation:
-//   S2 First-CC   k_chunk_rows, k_cc_local (shared-memory union-find per id block),
+//   S2 First-CC   k_cc_local (shared-memory union-find per id block; chunk row partition),
 //                 k_cc_sample, k_compress, k_giant, k_cc_rest(+heavy)
 //                 union-find; the edge that wins each hook CAS is recorded (HAB) = forest
 //   S3 rooting    k_arc_link, k_arc_close (root chain, isolated slots), ruling-set list ranking (k_lr_walk1,
@@ -202,9 +202,12 @@ __device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
 
 // It also initialises its block's hook records and out-arc heads (no separate init pass;
 // P is published for every id below, and Last-CC's C by k_cc2_local).
+// It also writes the warp-chunk row partition: CROW[c] = the nonempty row holding slot
+// c * WCH, from the row's own offsets (no per-chunk binary search; a hub row writes the
+// entries of all the chunks that start inside it).
 __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restrict__ off,
                                                       const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
-                                                      u32* HEAD) {
+                                                      u32* HEAD, u32* CROW) {
     __shared__ u32 sp[LOCAL_B];
     const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
     const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
@@ -216,6 +219,8 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restri
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
         i64 v = b0 + i, a = off[v], b = off[v + 1];
+        if (CROW)
+            for (i64 c = cdiv(a, WCH); c * WCH < b; ++c) CROW[c] = (u32)v;
         for (int k = 0; k < NSAMPLE && a + k < b; ++k) {
             i64 w = tgt[a + k];
             if ((w >> LOCAL_LB) != blockIdx.x) continue;
@@ -1423,8 +1428,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    if (w.nch > 0) PG_K(k_chunk_rows<<<nblk(w.nch, B), B, 0, st>>>(off, n, m, w.nch, w.CROW));
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, w.CROW));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
     PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
@@ -1537,7 +1541,7 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     const int B = 256;
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     if (n > 0) {
-        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD);
+        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, nullptr);
         k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB);
         k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
