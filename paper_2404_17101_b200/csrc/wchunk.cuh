@@ -154,31 +154,6 @@ struct BlkRows {
     bool last_open;    // (warp-uniform) the chunk's last row may continue past s1
 };
 
-// targets of the lane's 8 slots (two 16-byte streaming loads when aligned and in range)
-__device__ __forceinline__ void blk_load(const int32_t* __restrict__ tgt, i64 s1, i64 sl, u32 (&t)[BLK_SPL]) {
-    if (sl + BLK_SPL <= s1 && ((reinterpret_cast<uintptr_t>(tgt) & 15) == 0)) {
-        const uint4 a = __ldcs(reinterpret_cast<const uint4*>(tgt + sl));
-        const uint4 b = __ldcs(reinterpret_cast<const uint4*>(tgt + sl) + 1);
-        t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
-        t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
-    } else {
-#pragma unroll
-        for (int i = 0; i < BLK_SPL; ++i) t[i] = sl + i < s1 ? (u32)__ldcs(tgt + sl + i) : 0u;
-    }
-}
-
-// the lane's 8 slot values, two 16-byte streaming stores when aligned and in range
-__device__ __forceinline__ void blk_store(u32* __restrict__ out, i64 s1, i64 sl, const u32 (&v)[BLK_SPL]) {
-    if (sl + BLK_SPL <= s1 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-        __stcs(reinterpret_cast<uint4*>(out + sl), make_uint4(v[0], v[1], v[2], v[3]));
-        __stcs(reinterpret_cast<uint4*>(out + sl) + 1, make_uint4(v[4], v[5], v[6], v[7]));
-    } else {
-#pragma unroll
-        for (int i = 0; i < BLK_SPL; ++i)
-            if (sl + i < s1) __stcs(out + sl + i, v[i]);
-    }
-}
-
 // Row starts of chunk [s0, s1) whose first slot lies in row `base` (the nonempty row
 // containing s0): the mask and the row id at each start, in sm.  Returns whether the
 // chunk's last row continues past s1.  All 32 lanes call it.
