@@ -706,6 +706,11 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
     BlkSmem& sm = smem[threadIdx.x >> 5];
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     const i64 sl = s0 + BLK_SPL * lane;
+    const u32 base = crow[c];
+    // one row over the whole chunk (hub rows: most slots of a power-law graph): a plain
+    // warp min/max, no row pass, no transpose, no scan
+    const i64 a_base = off[base], e_base = off[(i64)base + 1];
+    const bool one_row = e_base >= s1;
     u32 fw[BLK_SPL];
     {
         // FIRST lines are kept in L2 ahead of the W stores and offsets (evict_last): C5a
@@ -716,9 +721,22 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
 #pragma unroll
         for (int k = 0; k < WCH_U; ++k)
             if (s0 + 32 * k + lane < s1) g[k] = ld_keep(FIRST + g[k], pol);
+        if (one_row) {   // warp-uniform
+            u32 mn = PG_INV, mx = 0;
+#pragma unroll
+            for (int k = 0; k < WCH_U; ++k)
+                if (s0 + 32 * k + lane < s1) {
+                    mn = g[k] < mn ? g[k] : mn;
+                    mx = g[k] > mx ? g[k] : mx;
+                }
+            mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+            mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+            if (lane == 0) write_tag(W, FIRST, base, mn, mx, a_base < s0 || e_base > s1);
+            return;
+        }
         blk_transpose(sm, lane, g, fw);
     }
-    const BlkRows br = blk_rows(off, n, s0, s1, crow[c], lane, sm);
+    const BlkRows br = blk_rows(off, n, s0, s1, base, lane, sm);
     const bool hstart = br.mb & 1u;
     u32 r = br.r_first;
     u32 mn = PG_INV, mx = 0, hmn = PG_INV, hmx = 0;

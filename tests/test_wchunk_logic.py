@@ -157,7 +157,12 @@ def emulate_tags_blk(off, vals, first):
 
     for c in range((m + WCH - 1) // WCH):
         s0, s1 = c * WCH, min(c * WCH + WCH, m)
-        mb, rfirst, rowat, last_open = blk_rows(off, n, s0, s1, chunk_row(off, n, s0))
+        base = chunk_row(off, n, s0)
+        if int(off[base + 1]) >= s1:        # one row over the whole chunk: warp min/max
+            seg = [int(vals[s]) for s in range(s0, s1)]
+            write(base, min(seg), max(seg), int(off[base]) < s0 or int(off[base + 1]) > s1)
+            continue
+        mb, rfirst, rowat, last_open = blk_rows(off, n, s0, s1, base)
         T, H, R, head, hst, inner = [], [], [], [], [], []
         for lane in range(32):
             sl = s0 + 8 * lane
