@@ -232,14 +232,75 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restri
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) P[b0 + i] = (u32)b0 + sfind(sp, (u32)i);
 }
 
-// sampled edges that cross blocks (the local phase took the rest)
+// sampled edges that cross blocks (the local phase took the rest).  The roots of v and of
+// its sampled neighbours are found in lockstep (independent pointer chains in flight
+// together), then the links are made one CAS each with the roots already known; a failed
+// CAS (another thread moved a root) falls back to the general uf_link_hook.  C5a First-CC
+// 11.3 -> 10.9 ms.
+template <int K>
+__device__ __forceinline__ void uf_find_lockstep(u32* P, u32 (&x)[K]) {
+    bool more = true;
+    while (more) {
+        more = false;
+        u32 p[K], gp[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) p[j] = ldcg(P + x[j]);
+#pragma unroll
+        for (int j = 0; j < K; ++j) gp[j] = p[j] != x[j] ? ldcg(P + p[j]) : p[j];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (p[j] == x[j]) continue;          // x[j] is a root
+            if (gp[j] != p[j]) {                 // path halving, as uf_find
+                stcg(P + x[j], gp[j]);
+                more = true;
+            }
+            x[j] = gp[j];
+        }
+    }
+}
+
 __global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     i64 a = off[v], b = off[v + 1];
-    for (int k = 0; k < NSAMPLE && a + k < b; ++k) {
-        u32 w = (u32)tgt[a + k];
-        if ((w >> LOCAL_LB) != (u32)(v >> LOCAL_LB)) uf_link_hook(P, (u32)v, w, HAB);
+    u32 t[NSAMPLE], x[NSAMPLE + 1];
+    bool act[NSAMPLE], any = false;
+    x[0] = (u32)v;
+#pragma unroll
+    for (int k = 0; k < NSAMPLE; ++k) {
+        act[k] = a + k < b;
+        t[k] = act[k] ? (u32)tgt[a + k] : (u32)v;
+        act[k] = act[k] && (t[k] >> LOCAL_LB) != (u32)(v >> LOCAL_LB);
+        x[k + 1] = act[k] ? t[k] : (u32)v;
+        any |= act[k];
+    }
+    if (!any) return;
+    uf_find_lockstep(P, x);
+    u32 rv = x[0], hooked[NSAMPLE], under[NSAMPLE];
+    int nh = 0;
+    bool fallback = false;
+#pragma unroll
+    for (int k = 0; k < NSAMPLE; ++k) {
+        if (!act[k]) continue;
+        if (fallback) {
+            uf_link_hook(P, (u32)v, t[k], HAB);
+            continue;
+        }
+        u32 rb = x[k + 1];
+        for (int j = 0; j < nh; ++j)           // a root this thread hooked now hangs under `under`
+            if (rb == hooked[j]) rb = under[j];
+        if (rb == rv) continue;
+        const u32 hi = rv > rb ? rv : rb, lo = rv ^ rb ^ hi;
+        if (atomicCAS(P + hi, hi, lo) == hi) {
+            HAB[2 * (size_t)hi] = make_uint2((u32)v, t[k]);
+            hooked[nh] = hi;
+            under[nh] = lo;
+            ++nh;
+            rv = lo;
+        } else {
+            uf_link_hook(P, (u32)v, t[k], HAB);
+            fallback = true;
+        }
     }
 }
 
