@@ -1018,9 +1018,17 @@ __global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __
         return;
     }
     uint2 fu = make_uint2((u32)i, E[i]);
-    for (i64 s = a; s < b; ++s) {
-        uint2 fw = FL[(u32)tgt[s]];
-        if (is_cross(fu, fw)) uf_link(C, (u32)i, fw.x);
+    // 4 slots at a time: their target loads, then their (first, last) gathers, in flight together
+    for (i64 s = a; s < b; s += 4) {
+        u32 w[4];
+        uint2 fw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = s + k < b ? (u32)tgt[s + k] : (u32)u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fw[k] = FL[w[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (s + k < b && is_cross(fu, fw[k])) uf_link(C, (u32)i, fw[k].x);
     }
 }
 
