@@ -306,25 +306,29 @@ __global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* _
 
 // Full compression.  A find is a chain of dependent loads, so each thread walks
 // COMPRESS_ILP chains in lockstep (positions v, v+stride, ...) to keep several in flight.
-constexpr int COMPRESS_ILP = 4;
+// First-CC's forest (after sampling: shallow trees under the hubs) compresses best with 4
+// chains per thread, Last-CC's (over preorder positions: longer chains) with 16 (sweep:
+// C5a Last-CC 12.2 -> 11.4 ms; First-CC is slower above 4).
+constexpr int COMPRESS_ILP = 4, COMPRESS_ILP2 = 16;
 
-__device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[COMPRESS_ILP], i64 (&idx)[COMPRESS_ILP]) {
+template <int ILP>
+__device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i64 (&idx)[ILP]) {
     const i64 stride = (i64)gridDim.x * blockDim.x;
     const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    u32 x[COMPRESS_ILP];
+    u32 x[ILP];
 #pragma unroll
-    for (int j = 0; j < COMPRESS_ILP; ++j) {
+    for (int j = 0; j < ILP; ++j) {
         idx[j] = t + j * stride;
         x[j] = idx[j] < n ? ldcg(P + idx[j]) : 0u;
     }
     bool more = true;
     while (more) {
         more = false;
-        u32 px[COMPRESS_ILP];
+        u32 px[ILP];
 #pragma unroll
-        for (int j = 0; j < COMPRESS_ILP; ++j) px[j] = idx[j] < n ? ldcg(P + x[j]) : x[j];
+        for (int j = 0; j < ILP; ++j) px[j] = idx[j] < n ? ldcg(P + x[j]) : x[j];
 #pragma unroll
-        for (int j = 0; j < COMPRESS_ILP; ++j) {
+        for (int j = 0; j < ILP; ++j) {
             if (px[j] != x[j]) {
                 x[j] = px[j];
                 more = true;
@@ -332,16 +336,17 @@ __device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[COMPRESS
         }
     }
 #pragma unroll
-    for (int j = 0; j < COMPRESS_ILP; ++j) {
+    for (int j = 0; j < ILP; ++j) {
         root[j] = x[j];
         if (idx[j] < n) stcg(P + idx[j], x[j]);
     }
 }
 
+template <int ILP>
 __global__ void k_compress(i64 n, u32* P) {
-    u32 root[COMPRESS_ILP];
-    i64 idx[COMPRESS_ILP];
-    compress_ilp(n, P, root, idx);
+    u32 root[ILP];
+    i64 idx[ILP];
+    compress_ilp<ILP>(n, P, root, idx);
 }
 
 // most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root)
@@ -1060,12 +1065,12 @@ __global__ void k_cc2_rest_heavy(i64 n, const i64* __restrict__ off, const int32
 
 // final roots over positions + component count
 __global__ void k_compress_final(i64 n, u32* C, Ctr* ctr) {
-    u32 root[COMPRESS_ILP];
-    i64 idx[COMPRESS_ILP];
-    compress_ilp(n, C, root, idx);
+    u32 root[COMPRESS_ILP2];
+    i64 idx[COMPRESS_ILP2];
+    compress_ilp<COMPRESS_ILP2>(n, C, root, idx);
     u32 cnt = 0;
 #pragma unroll
-    for (int j = 0; j < COMPRESS_ILP; ++j) cnt += __popc(__ballot_sync(0xFFFFFFFFu, idx[j] < n && root[j] == (u32)idx[j]));
+    for (int j = 0; j < COMPRESS_ILP2; ++j) cnt += __popc(__ballot_sync(0xFFFFFFFFu, idx[j] < n && root[j] == (u32)idx[j]));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr->ncomp, cnt);
 }
 
@@ -1517,7 +1522,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // ---- S2 First-CC
     PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, w.CROW));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
-    PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
+    PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
     PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
@@ -1563,11 +1568,11 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // ---- S5 Last-CC over cross edges
     PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
     PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
-    PG_K(k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C));
+    PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
-    PG_K(k_compress_final<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.C, w.ctr));
+    PG_K(k_compress_final<<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C, w.ctr));
     PG_K(k_cid_vertices<<<nblk(n, B), B, 0, st>>>(n, w.C, w.FIRST, w.ctr, w.CIDV, w.GBIT, out->comp));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
@@ -1630,11 +1635,11 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     if (n > 0) {
         k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, nullptr);
         k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB);
-        k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
+        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
         k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
         k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
-        k_compress<<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
+        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
     }
     k_cc_count<<<1, 1, 0, st>>>(w.ctr, count_dev);
