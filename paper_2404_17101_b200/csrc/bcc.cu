@@ -1148,6 +1148,9 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
 // cross edge joins one component.  Most slots of a power-law graph point into the giant
 // component, so the target's component comes from the L2-resident membership bitmap and
 // only the remaining slots gather CIDV from HBM.
+#ifndef PG_LABELS_HALVES
+#define PG_LABELS_HALVES 4
+#endif
 __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
                                                       const u32* __restrict__ CIDV, const u32* __restrict__ GBIT,
@@ -1157,41 +1160,47 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
     if (c >= num_chunks(m)) return;
     const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
     const u32 g = ctr->gcid;
-    u32 w[WCH_U], cw[WCH_U], rw[WCH_U];
+    u32 w[WCH_U];
 #pragma unroll
     for (int k = 0; k < WCH_U; ++k) {
         i64 s = s0 + 32 * k + lane;
         w[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
     }
-    // rows of all windows first: the offset loads and shuffles overlap the target loads
+    // the chunk in PG_LABELS_HALVES parts: fewer live registers (32 per thread, no spills)
+    constexpr int H = WCH_U / PG_LABELS_HALVES;
     u32 cur = crow[c];
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        rw[k] = 0;
-        const i64 sb = s0 + 32 * k;
-        if (sb < s1) {   // warp-uniform
-            rw[k] = wc_resolve_row(off, n, cur, sb, lane, sb + lane < s1);
-            cur = __shfl_sync(0xFFFFFFFFu, rw[k], 31);
+    for (int h = 0; h < WCH_U; h += H) {
+        u32 cw[H], rw[H];
+        // rows of the part's windows first: the offset loads and shuffles overlap the gathers
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+            rw[k] = 0;
+            const i64 sb = s0 + 32 * (h + k);
+            if (sb < s1) {   // warp-uniform
+                rw[k] = wc_resolve_row(off, n, cur, sb, lane, sb + lane < s1);
+                cur = __shfl_sync(0xFFFFFFFFu, rw[k], 31);
+            }
         }
-    }
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        i64 s = s0 + 32 * k + lane;
-        cw[k] = s < s1 ? __ldg(GBIT + (w[k] >> 5)) : 0u;
-    }
+        for (int k = 0; k < H; ++k) {
+            i64 s = s0 + 32 * (h + k) + lane;
+            cw[k] = s < s1 ? __ldg(GBIT + (w[h + k] >> 5)) : 0u;
+        }
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        i64 s = s0 + 32 * k + lane;
-        cw[k] = (cw[k] >> (w[k] & 31)) & 1u ? g : (s < s1 ? __ldg(CIDV + w[k]) : 0u);
-    }
+        for (int k = 0; k < H; ++k) {
+            i64 s = s0 + 32 * (h + k) + lane;
+            cw[k] = (cw[k] >> (w[h + k] & 31)) & 1u ? g : (s < s1 ? __ldg(CIDV + w[h + k]) : 0u);
+        }
 #pragma unroll
-    for (int k = 0; k < WCH_U; ++k) {
-        const i64 s = s0 + 32 * k + lane;
-        if (s >= s1) break;
-        u32 cu = __ldg(CIDV + rw[k]);
-        u32 lab = cu > cw[k] ? cu : cw[k];
-        if (w[k] == rw[k]) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
-        __stcs(label + s, lab);
+        for (int k = 0; k < H; ++k) {
+            const i64 s = s0 + 32 * (h + k) + lane;
+            if (s >= s1) break;
+            u32 cu = __ldg(CIDV + rw[k]);
+            u32 lab = cu > cw[k] ? cu : cw[k];
+            if (w[h + k] == rw[k]) lab = PG_INV;  // self-loop: unlabelled, as in the reference (-1)
+            __stcs(label + s, lab);
+        }
     }
 }
 
