@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
 #pragma unroll
         for (int k = 0; k < H; ++k) {
             i64 s = s0 + 32 * (h + k) + lane;
-            cw[k] = (cw[k] >> (w[h + k] & 31)) & 1u ? g : (s < s1 ? __ldg(CIDV + w[h + k]) : 0u);
+            cw[k] = (cw[k] >> (w[h + k] & 31)) & 1u ? g : (s < s1 ? ld_na(CIDV + w[h + k]) : 0u);
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {

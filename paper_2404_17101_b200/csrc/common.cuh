@@ -34,9 +34,17 @@ __device__ __forceinline__ u64 policy_evict_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// (no L1 allocation: random gathers have no L1 reuse, and the L1 lines they would take
+// hold other warps' in-flight data; C5a tags 36.7 -> 36.2 ms)
 __device__ __forceinline__ u32 ld_keep(const u32* p, u64 pol) {
     u32 r;
-    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// random read-only gather without L1 allocation
+__device__ __forceinline__ u32 ld_na(const u32* p) {
+    u32 r;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ void stcg(u32* p, u32 v) { __stcg(p, v); }
