@@ -120,7 +120,12 @@ __global__ void k_set_scalar(T* p, T v) { *p = v; }
 // the total (if requested) is set to the identity.
 template <class T, class Op, class LoadF, class StoreF>
 cudaError_t launch_scan(i64 nitems, u64* status, T identity, Op op, LoadF load, StoreF store,
-                        T* total_out, cudaStream_t stream) {
+                        T* total_out, cudaStream_t stream, int carveout = -1) {
+    if (carveout >= 0) {   // shared-memory carveout preference (percent) of this instantiation
+        cudaError_t e = cudaFuncSetAttribute(k_scan<T, Op, LoadF, StoreF>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+        if (e != cudaSuccess) return e;
+    }
     if (nitems <= 0) {
         if (total_out) k_set_scalar<T><<<1, 1, 0, stream>>>(total_out, identity);
         return cudaGetLastError();
