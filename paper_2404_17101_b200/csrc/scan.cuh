@@ -22,8 +22,9 @@ constexpr int SCAN_BLOCK = 256;
 #endif
 constexpr int SCAN_IPT = PG_SCAN_IPT;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_IPT;
-// 8 resident tiles per SM (32 registers): without the bound the preorder scan took 56
-// registers and ran 4 tiles per SM (C5a tour 10.5 -> 9.8 ms, C3 0.65 -> 0.50)
+// 32-bit scans: 8 resident tiles per SM (32 registers): without the bound the preorder scan took 56
+// registers and ran 4 tiles per SM (C5a tour 10.5 -> 9.8 ms, C3 0.65 -> 0.50).  64-bit scans
+// (CSR builder, loaders) keep the compiler's choice: at 32 registers they spill.
 #ifndef PG_SCAN_MINB
 #define PG_SCAN_MINB 8
 #endif
@@ -42,7 +43,7 @@ struct MinOp {
 inline size_t scan_status_bytes(i64 nitems) { return sizeof(u64) * (size_t)(cdiv(nitems, SCAN_TILE) + 2); }
 
 template <class T, class Op, class LoadF, class StoreF>
-__global__ void __launch_bounds__(SCAN_BLOCK, PG_SCAN_MINB)
+__global__ void __launch_bounds__(SCAN_BLOCK, sizeof(T) == 4 ? PG_SCAN_MINB : 1)
 k_scan(i64 nitems, u64* status, T identity, Op op, LoadF load, StoreF store, T* total_out) {
     typedef cub::BlockScan<T, SCAN_BLOCK> BS;
     __shared__ typename BS::TempStorage tmp;
