@@ -342,8 +342,13 @@ __device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i6
     }
 }
 
+// 16 chains per thread took 140 registers (one 256-thread block per SM); capped at 128, two
+// blocks fit without spills (C5a Last-CC -0.1..0.3 ms)
+#ifndef PG_CMP_MINB
+#define PG_CMP_MINB 2
+#endif
 template <int ILP>
-__global__ void k_compress(i64 n, u32* P) {
+__global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i64 n, u32* P) {
     u32 root[ILP];
     i64 idx[ILP];
     compress_ilp<ILP>(n, P, root, idx);
@@ -1064,7 +1069,7 @@ __global__ void k_cc2_rest_heavy(i64 n, const i64* __restrict__ off, const int32
 }
 
 // final roots over positions + component count
-__global__ void k_compress_final(i64 n, u32* C, Ctr* ctr) {
+__global__ void __launch_bounds__(256, PG_CMP_MINB) k_compress_final(i64 n, u32* C, Ctr* ctr) {
     u32 root[COMPRESS_ILP2];
     i64 idx[COMPRESS_ILP2];
     compress_ilp<COMPRESS_ILP2>(n, C, root, idx);
