@@ -1534,7 +1534,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
 #ifndef PG_TAGS_CARVE
 #define PG_TAGS_CARVE 25
 #endif
-    PG_CUDA_TRY(cudaFuncSetAttribute(k_tags_blk, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
+    if (PG_TAGS_CARVE >= 0)
+        PG_CUDA_TRY(cudaFuncSetAttribute(k_tags_blk, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
     PG_CUDA_TRY(mark(PASGAL_STAGE_BEGIN));
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     PG_CUDA_TRY(cudaMemsetAsync(out->artic_bits, 0, sizeof(u32) * (size_t)cdiv(n, 32), st));
