@@ -766,6 +766,9 @@ __device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u
 #ifndef PG_TAGS_MINB
 #define PG_TAGS_MINB 6
 #endif
+// NOL1: the FIRST gathers skip L1 (large graphs: no reuse, and L1 holds in-flight misses);
+// below 2^22 vertices FIRST (<= 16 MB) partly lives in L1 and the plain load is faster
+template <bool NOL1>
 __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64* __restrict__ off,
                                                                 const int32_t* __restrict__ tgt, i64 n, i64 m,
                                                                 const u32* __restrict__ crow,
@@ -791,7 +794,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
         wc_load(tgt, m, c, lane, g);
 #pragma unroll
         for (int k = 0; k < WCH_U; ++k)
-            if (s0 + 32 * k + lane < s1) g[k] = ld_keep(FIRST + g[k], pol);
+            if (s0 + 32 * k + lane < s1) g[k] = NOL1 ? ld_keep(FIRST + g[k], pol) : ld_keep_l1(FIRST + g[k], pol);
         if (one_row) {   // warp-uniform
             u32 mn = PG_INV, mx = 0;
 #pragma unroll
@@ -1535,7 +1538,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
 #define PG_TAGS_CARVE 25
 #endif
     if (PG_TAGS_CARVE >= 0)
-        PG_CUDA_TRY(cudaFuncSetAttribute(k_tags_blk, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
+        PG_CUDA_TRY(cudaFuncSetAttribute(k_tags_blk<true>, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
     PG_CUDA_TRY(mark(PASGAL_STAGE_BEGIN));
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     PG_CUDA_TRY(cudaMemsetAsync(out->artic_bits, 0, sizeof(u32) * (size_t)cdiv(n, 32), st));
@@ -1583,7 +1586,12 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
-    if (w.nch > 0) PG_K(k_tags_blk<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+    if (w.nch > 0) {
+        if (n >= ((i64)1 << 22))
+            PG_K(k_tags_blk<true><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+        else
+            PG_K(k_tags_blk<false><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+    }
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));

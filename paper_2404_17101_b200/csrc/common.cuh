@@ -41,6 +41,11 @@ __device__ __forceinline__ u32 ld_keep(const u32* p, u64 pol) {
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
+__device__ __forceinline__ u32 ld_keep_l1(const u32* p, u64 pol) {
+    u32 r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
 // random read-only gather without L1 allocation
 __device__ __forceinline__ u32 ld_na(const u32* p) {
     u32 r;
