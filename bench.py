@@ -42,8 +42,9 @@ def b_alg_pipeline(n, m):
 KERNEL_BYTES = {
     # k_tags: per slot target 4 + first[w] 4; per vertex offsets 8 + first[u] 4 + w1/w2 write 8
     "tags": lambda n, m: 8 * m + 20 * n,
-    # k_labels: per slot target 4 + (first,comp)[w] 8 + label write 4; per vertex offsets 8 + (first,comp)[u] 8
-    "labels": lambda n, m: 16 * m + 16 * n,
+    # k_labels: per slot target 4 + CID[w] 4 (one gather; the giant bitmap only avoids some of
+    # them) + label write 4; per vertex offsets 8 + CID[u] 4
+    "labels": lambda n, m: 12 * m + 12 * n,
 }
 KERNEL_NAMES = {"tags": "k_tags_blk", "labels": "k_labels"}
 
@@ -206,19 +207,13 @@ def random_access_roofline(traffic, kernel_ms):
 
 SAMPLE_DESC = ("RMAT scale 20, 2^24 draws, (a,b,c)=(.57,.19,.19), seed 1 -- the same generator "
                "rules as the bench workload at 1/256 of its size (= BASELINE configs[1])")
+SAMPLE_CONFIG = "c2"
 
 
-def cpu_sample_graph(use_gpu):
-    import numpy as np
-
-    if use_gpu:
-        import paper_2404_17101_b200 as pg
-
-        dg = pg.gen_rmat(20, 1 << 24, seed=1)
-        off = dg.offsets.cpu().numpy()
-        tgt = dg.targets.cpu().numpy().view(np.uint32)
-        del dg
-        return off, tgt
+def cpu_sample_graph():
+    """The bounded CPU sample (BASELINE configs[1]), built on the host by the generator twin
+    (oracle/gen_host.c; equal to the device generator's output, tests/test_oracle.py), so the
+    reference arm never loads libpasgal_bcc.so."""
     import oracle
 
     return oracle.rmat(20, 1 << 24, seed=1)
@@ -245,6 +240,51 @@ def oracle_rate(off, tgt, threads=1):
     return time.perf_counter() - t0, mu * threads
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def _python_reference_worker(args):
+    """One process: the UNMODIFIED reference (baseline/_ref, pip-installed from the
+    reference package) -- pasgal.oracles.bcc_hopcroft_tarjan (oracles.py:119-201) -- on C1."""
+    off, tgt, reps = args
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from pasgal.graph import Graph
+    from pasgal.oracles import bcc_hopcroft_tarjan
+
+    g = Graph(off, tgt)
+    bcc_hopcroft_tarjan(g)                      # warm-up (imports, numba-free path)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        r = bcc_hopcroft_tarjan(g)
+    return time.perf_counter() - t0, int(r.bcc_count)
+
+
+def python_reference_rate(procs, reps=3):
+    """The reference's own Python CPU path on BASELINE configs[0] (C1, grid 256^2 p=0.6,
+    the reference's CPU-runnable case), `procs` concurrent processes, or None when
+    baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "pasgal")):
+        return None
+    import multiprocessing as mp
+
+    import oracle
+
+    off, tgt = oracle.gen_grid(256, 256, 0.6, 1)
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_python_reference_worker, [(off, tgt, reps)] * procs)
+    wall = time.perf_counter() - t0
+    per = max(r[0] for r in res)
+    mu = tgt.shape[0] // 2
+    return {"value": mu * reps * procs / per, "unit": UNIT, "cores": procs, "kind": "reference",
+            "config": "c1: grid 256x256, p=0.6, seed 1 (BASELINE configs[0])",
+            "bcc_count": res[0][1], "seconds_per_call": per / reps, "wall_s": round(wall, 1),
+            "path": "pasgal.oracles.bcc_hopcroft_tarjan from baseline/_ref (pip install --no-deps of "
+                    "/root/reference/pkg), unmodified; one instance per process"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -252,13 +292,7 @@ def run_reference(args, rank, world):
 
     oracle.build()
     cores = os.cpu_count() or 1
-    try:
-        import torch
-
-        use_gpu = torch.cuda.is_available()
-    except Exception:
-        use_gpu = False
-    off, tgt = cpu_sample_graph(use_gpu)
+    off, tgt = cpu_sample_graph()
     for _ in range(args.warmup):
         oracle_rate(off, tgt, cores)
     times, edges = [], 0
@@ -268,14 +302,25 @@ def run_reference(args, rank, world):
         edges += e
     total = sum(times)
     value = edges / total
+    pyref = None
+    try:
+        pyref = python_reference_rate(cores)
+    except Exception as e:  # noqa: BLE001 -- reported, the C-port line stands
+        pyref = {"unavailable": f"{type(e).__name__}: {e}"}
+    cfg = workload_config(SAMPLE_CONFIG)
+    cfg.update(n=int(off.shape[0] - 1), m_slots=int(tgt.shape[0]),
+               sample_of=workload_config(args.config)["workload"],
+               note=f"a bounded sample of the GPU arm's workload: the same generator rules at 1/256 of its size")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": workload_config(args.config),
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{SAMPLE_DESC}; {cores} concurrent instances per step (one per host thread)"},
+                         "sample": f"{SAMPLE_DESC}; {cores} concurrent instances per step (one per host thread) "
+                                   "of oracle/bcc_oracle.c, the C restatement of bcc_hopcroft_tarjan"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "python_reference": pyref,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -378,6 +423,21 @@ def run_ours(args, rank, world, local):
                 "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
                 "stage_share": {k: round(v / statistics.mean(step_ms), 4) for k, v in stage_ms.items()}}
 
+    # ---- run checksum of the LAST TIMED step's output (outside the timed region): its raw
+    # labels canonicalised on the device, checksummed, and compared with the value pinned
+    # from the oracle-verified output of the same CSR (tests/golden/c5a_oracle_hashes.json)
+    run_checksum = None
+    if not args.no_checksum:
+        canon = pg.canonicalize_device(dg.offsets, dg.targets, out.edge_label, label_bound=max(n, 1))
+        cs = pg.canonical_checksum_device(canon, out.artic_bits, out.bcc_count)
+        del canon
+        torch.cuda.empty_cache()
+        pinned = pinned_checksum(args.config, cfg_seed, n, m)
+        run_checksum = {"value": [str(x) for x in cs], "pinned": pinned,
+                        "match": (None if pinned is None else [str(x) for x in cs] == pinned),
+                        "rule": "(bcc_count, articulation points, sum canon[s]*(((s*0x9E3779B1) mod 2^32)|1) "
+                                "mod 2^64) of the last timed step's labels, canonicalised after the timing"}
+
     # ---- e2e through the public drop-in call with host buffers (pinned), H2D + D2H timed
     e2e = None
     if not args.no_e2e:
@@ -402,11 +462,17 @@ def run_ours(args, rank, world, local):
         import oracle
 
         oracle.build()
-        off_s, tgt_s = cpu_sample_graph(True)
+        off_s, tgt_s = cpu_sample_graph()
         dt, e = oracle_rate(off_s, tgt_s, 1)
         cpu = {"value": e / dt, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{SAMPLE_DESC}; one run of the C restatement of bcc_hopcroft_tarjan "
                          f"(incl. its is_symmetric + twin passes), {dt:.2f} s"}
+
+    # ---- the other BASELINE configs, device-timed (L2 flushed between steps), and the CPU
+    # sample config through bcc(g) end to end: a like-for-like pair for the reference arm
+    per_config = same_config = None
+    if not args.no_per_config and args.config == "c5a":
+        per_config, same_config = run_per_config(args, dev, world)
 
     if rank == 0:
         line = {
@@ -425,11 +491,100 @@ def run_ours(args, rank, world, local):
             "gpu_launches": launches,
             "clocks": clocks,
             "window_ms": window_ms,
+            "run_checksum": run_checksum,
+            "per_config": per_config,
+            "same_config": same_config,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def pinned_checksum(config, seed, n, m):
+    """The canonical checksum pinned for (config, seed) in tests/golden/*_oracle_hashes.json
+    (written from an output whose full labels hashed equal to the oracle's), else None."""
+    try:
+        with open(os.path.join(REPO, "tests", "golden", f"{config}_oracle_hashes.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    if d.get("n") != n or d.get("m_slots") != m or "checksum" not in d or d.get("seed", 1) != seed:
+        return None
+    return [str(x) for x in d["checksum"]]
+
+
+def time_device(pg, torch, dg, steps, warmup, seed=0):
+    """Mean device ms of one pasgal_bcc call on a resident CSR, L2 flushed between steps."""
+    n, m = dg.n, dg.m
+    ws = torch.empty(pg.workspace_bytes(n, m), dtype=torch.uint8, device=dg.offsets.device)
+    out = pg.DeviceBcc(edge_label=torch.empty(max(m, 1), dtype=torch.int32, device=ws.device),
+                       artic_bits=torch.empty(max((n + 31) // 32, 1), dtype=torch.int32, device=ws.device),
+                       bcc_count=torch.empty(1, dtype=torch.int64, device=ws.device))
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=ws.device)
+    for _ in range(warmup):
+        flush.fill_(1)
+        pg.bcc_device(dg.offsets, dg.targets, seed=seed, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    tot = 0.0
+    launches = 0
+    for k in range(steps):
+        flush.fill_(k)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        launches += pg.bcc_device(dg.offsets, dg.targets, seed=seed, out=out, workspace=ws).launches
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot / steps, launches // steps
+
+
+def run_per_config(args, dev, world):
+    """Device time of C1-C4 (each: generate, warm up, time, free) and the CPU sample config
+    (C2) through the public bcc(g) with pinned host buffers -- the reference arm's config."""
+    import torch
+
+    import paper_2404_17101_b200 as pg
+
+    per = {}
+    same = None
+    for name in ("c1", "c2", "c3", "c4"):
+        dg = pg.make_config(name, device=dev)
+        torch.cuda.synchronize()
+        ms, nl = time_device(pg, torch, dg, steps=10, warmup=3)
+        if world > 1:
+            import torch.distributed as dist
+
+            ms = _allreduce([ms], dist.ReduceOp.MAX, dev)[0]
+        per[name] = {"ms": round(ms, 4), "edges_per_s": (dg.m // 2) / (ms / 1e3), "n": dg.n, "m_slots": dg.m,
+                     "launches": nl}
+        if name == SAMPLE_CONFIG:
+            off_h = torch.empty(dg.n + 1, dtype=torch.int64, pin_memory=True)
+            tgt_h = torch.empty(dg.m, dtype=torch.int32, pin_memory=True)
+            off_h.copy_(dg.offsets)
+            tgt_h.copy_(dg.targets)
+            g = pg.Graph(off_h.numpy(), tgt_h.numpy())
+            hb = pg.HostBuffers.allocate(dg.n, dg.m)
+            for _ in range(3):
+                pg.bcc(g, device=dev, host_out=hb)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps = 10
+            for _ in range(reps):
+                r = pg.bcc(g, device=dev, host_out=hb)
+            e2e_s = (time.perf_counter() - t0) / reps
+            same = {"config": workload_config(name)["workload"],
+                    "device": {"value": (dg.m // 2) / (ms / 1e3), "unit": UNIT, "ms_per_step": round(ms, 4)},
+                    "e2e": {"value": (dg.m // 2) / e2e_s, "unit": UNIT, "ms_per_step": round(e2e_s * 1e3, 3),
+                            "h2d_bytes_per_step": 8 * (dg.n + 1) + 4 * dg.m,
+                            "d2h_bytes_per_step": 4 * dg.m + dg.n + 8, "bcc_count": int(r.bcc_count),
+                            "path": "paper_2404_17101_b200.bcc(g): H2D, validate, FAST-BCC, D2H (pinned)"},
+                    "note": "the reference arm's config (bench.py --impl reference times its CPU path on it)"}
+            del hb, g, off_h, tgt_h, r
+        del dg
+        pg.release_workspace()
+        torch.cuda.empty_cache()
+    return per, same
 
 
 def run_batch(args, rank, world, local):
@@ -456,9 +611,11 @@ def run_batch(args, rank, world, local):
     S = max(1, min(args.streams, len(graphs)))
     streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
     wss = [torch.empty(pg.workspace_bytes(nmax, mmax), dtype=torch.uint8, device=dev) for _ in range(S)]
-    outs = [pg.DeviceBcc(edge_label=torch.empty(mmax, dtype=torch.int32, device=dev),
-                         artic_bits=torch.empty((nmax + 31) // 32, dtype=torch.int32, device=dev),
-                         bcc_count=torch.empty(1, dtype=torch.int64, device=dev)) for _ in range(S)]
+    # one output per instance (a workspace per stream): the outputs of the last timed step
+    # are the ones checksummed and verified below
+    outs = [pg.DeviceBcc(edge_label=torch.empty(g.m, dtype=torch.int32, device=dev),
+                         artic_bits=torch.empty((g.n + 31) // 32, dtype=torch.int32, device=dev),
+                         bcc_count=torch.empty(1, dtype=torch.int64, device=dev)) for g in graphs]
     launches = 0
     main_stream = torch.cuda.current_stream(dev)
 
@@ -471,7 +628,7 @@ def run_batch(args, rank, world, local):
         for i, g in enumerate(graphs):
             k = i % S
             with torch.cuda.stream(streams[k]):
-                nl += pg.bcc_device(g.offsets, g.targets, out=outs[k], workspace=wss[k]).launches
+                nl += pg.bcc_device(g.offsets, g.targets, out=outs[i], workspace=wss[k]).launches
         for st in streams:
             e = torch.cuda.Event()
             e.record(st)
@@ -497,12 +654,14 @@ def run_batch(args, rank, world, local):
     total_ms = e0.elapsed_time(e1)
     mu = sum(g.m // 2 for g in graphs) * args.steps
     total_ms, edges = reduce_over_ranks(total_ms, mu, dev)
-    # per-instance canonical checksums (outside the timed region), and on rank 0
-    # the first --verify instances re-run by the C oracle on the host threads
+    # per-instance canonical checksums of the outputs the LAST TIMED step wrote (
+    # canonicalised after the timing), and on rank 0 the first --verify instances re-run by
+    # the C oracle on the host threads
     sums = []
-    for g in graphs:
-        r = pg.bcc_device(g.offsets, g.targets, canonical=True, out=outs[0], workspace=wss[0])
-        sums.append(pg.canonical_checksum_device(r.edge_label[:g.m], r.artic_bits[:(g.n + 31) // 32], r.bcc_count))
+    for i, g in enumerate(graphs):
+        canon = pg.canonicalize_device(g.offsets, g.targets, outs[i].edge_label, label_bound=max(g.n, 1))
+        sums.append(pg.canonical_checksum_device(canon, outs[i].artic_bits, outs[i].bcc_count))
+        del canon
     verified = None
     if rank == 0 and args.verify > 0:
         verified = verify_instances([graphs[i] for i in range(min(args.verify, len(graphs)))],
@@ -518,8 +677,9 @@ def run_batch(args, rank, world, local):
                        "instances_per_s": args.instances * args.steps / (total_ms / 1e3),
                        "l2": "inputs larger than L2 (batch of 64 x 295 MB CSR)"},
             "gpu_launches": launches, "clocks": clocks,
-            "checksums": {"instances": [mine[i] + 1 for i in range(len(sums))][:8],
-                          "bcc_count_art_hash": [list(map(str, c)) for c in sums[:8]],
+            "checksums": {"instances": [mine[i] + 1 for i in range(len(sums))],
+                          "bcc_count_art_hash": [list(map(str, c)) for c in sums],
+                          "of": "the outputs of the last timed concurrent step (one output buffer per instance)",
                           "rule": "(bcc_count, articulation points, sum canon[s]*(((s*0x9E3779B1) mod 2^32)|1) mod 2^64)"},
             "verified": verified,
         }
@@ -664,6 +824,45 @@ def run_e2e(args, off_h, tgt_h, dev, n, m, participate=True, k=1, world=1):
     return out
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 with the same arguments; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """The launch path without a GPU (gloo): every rank reports the replica seed and the
+    c5b instances it would run; rank 0 prints them.  Used by tests/test_replicas.py."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    import paper_2404_17101_b200.graph as gmod
+
+    seed = gmod.CONFIGS[args.config]["seed"] + rank if args.config in gmod.CONFIGS else 1 + rank
+    mine = assign_instances(args.instances, rank, world)
+    rec = torch.tensor([rank, seed, len(mine), sum(mine)], dtype=torch.int64)
+    allr = [torch.zeros_like(rec) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allr, rec)
+    else:
+        allr = [rec]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_arg": args.gpus,
+                          "ranks": [r.tolist() for r in allr], "config": args.config}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -678,8 +877,17 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-checksum", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launch path only (gloo, no GPU)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.config == "c5b":

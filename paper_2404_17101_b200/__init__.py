@@ -12,12 +12,12 @@ from .bcc import (DeviceBcc, HostBuffers, canonical_checksum_device, canonicaliz
                   same_partition_device)
 from .bcc import articulation_bytes_device, bcc, bcc_device, release_workspace, unpack_articulation, validate_device, validate_workspace_bytes, workspace_bytes
 
-from .io import GraphFormatError, load_adj, load_bin, save_adj, save_bin
+from .io import GraphFormatError, load_adj, load_bin, load_graph, save_adj, save_bin
 from .pipeline import BccPipeline
 from .bfs import UNREACHED, DistanceArray, GraphStats, bfs, eccentricities, estimate_diameter
 
 __all__ = [
-    "GraphFormatError", "load_adj", "load_bin", "save_adj", "save_bin",
+    "GraphFormatError", "load_adj", "load_bin", "load_graph", "save_adj", "save_bin",
     "BccPipeline", "UNREACHED", "DistanceArray", "GraphStats", "bfs", "eccentricities", "estimate_diameter",
     "BccLabels", "canonical_checksum", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
     "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",

@@ -107,6 +107,21 @@ static inline i64 rmq_levels(i64 nb) {
     return lv;
 }
 
+// Ruler-array capacity: the default spacing coarsens as n grows (lr_shift), so a graph
+// just below a threshold can need more rulers than one just above it.  Sizing for the
+// largest count any n' <= n needs keeps pasgal_bcc_workspace_bytes non-decreasing in n, so
+// a workspace sized for the largest graph of a batch fits every smaller one.
+static inline i64 ruler_capacity(i64 n, i64 ns) {
+    const i64 T[3] = {(i64)1 << 18, (i64)1 << 25, (i64)1 << 28};
+    const int S[3] = {3, 4, 6};
+    for (int k = 0; k < 3; ++k)
+        if (n >= T[k]) {
+            const i64 c = cdiv(2 * (T[k] - 1), (i64)1 << S[k]) + 1;
+            if (c > ns) ns = c;
+        }
+    return ns;
+}
+
 static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     size_t o = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -121,6 +136,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.lv = rmq_levels(w.nb);
     w.lrs = (u32)lr_shift(n);
     w.ns = cdiv(L, (i64)1 << w.lrs) + 1;   // + the head ruler
+    const i64 ns_cap = ruler_capacity(n, w.ns);
     w.nch = num_chunks(m);
     i64 scan_items = L > m ? L : m;
     w.P = (u32*)take(4 * nn);
@@ -128,8 +144,8 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.HEAD = (u32*)take(4 * nn);
     w.NEXT = (u32*)take(4 * L);
     for (int b = 0; b < 2; ++b) {
-        w.SPLEN[b] = (u32*)take(4 * w.ns);
-        w.SPNEXT[b] = (u32*)take(4 * w.ns);
+        w.SPLEN[b] = (u32*)take(4 * ns_cap);
+        w.SPNEXT[b] = (u32*)take(4 * ns_cap);
     }
     w.TA = (u32*)take(4 * L);
     w.TP = (u32*)take(4 * L);

@@ -8,7 +8,9 @@ offsets, m u32 targets) and its text adjacency format load_adj / save_adj
 truncation and size-field mismatches; the offset and target arrays go straight to HBM
 and their range checks run on the device, which reports the first offending index so the
 error names the same byte position the reference would.  The BCC path is unweighted:
-a ``.wbin`` file's trailing weight block is validated for length and ignored.
+a ``.wbin`` file's trailing weight block is validated (length, and the reference's
+negative-weight error, graph.py:384-390, checked on the device) and not returned.
+``load_graph`` dispatches on the extension like graph.py:411-418.
 """
 
 import ctypes
@@ -46,6 +48,8 @@ def load_bin(path, device="cuda"):
     n, m, size_field = struct.unpack_from("<QQQ", mm[:_HDR].tobytes(), 0)
     if n >= 2 ** 31:
         raise GraphFormatError(f"vertex count {n} exceeds the int32 vertex ids of the device CSR", path, byte=0)
+    if m >= 2 ** 32:
+        raise GraphFormatError(f"edge count {m} exceeds the uint32 slot ids of the device CSR", path, byte=8)
     base = _HDR + (n + 1) * 8 + m * 4
     if size_field != base:
         raise GraphFormatError(f"size-field mismatch: header says {size_field}, layout needs {base}", path, byte=16)
@@ -76,7 +80,25 @@ def load_bin(path, device="cuda"):
         t = int(tgt_np[i])
         raise GraphFormatError(f"target out of range at edge {i}: {t} >= n={n}", path,
                                byte=_HDR + (n + 1) * 8 + i * 4)
+    if path.suffix == ".wbin" and m:
+        # graph.py:384-390 tests weights.min() < 0: -0.0 passes, and numpy's min propagates
+        # NaN, so a block holding any NaN passes whatever else it holds
+        w = torch.from_numpy(np.frombuffer(mm, dtype="<f4", count=m, offset=base).copy()).to(device)
+        neg = torch.nonzero(w < 0)
+        if neg.numel() and not bool(torch.isnan(w).any().item()):
+            i = int(neg[0, 0].item())
+            raise GraphFormatError(f"negative weight at edge {i}", path, byte=base + i * 4)
     return DeviceGraph(off, tgt)
+
+
+def load_graph(path, weighted=None, device="cuda"):
+    """Dispatch on extension (graph.py:411-418): .adj -> load_adj, .bin/.wbin -> load_bin."""
+    p = Path(path)
+    if p.suffix == ".adj":
+        return load_adj(p, weighted, device=device)
+    if p.suffix in (".bin", ".wbin"):
+        return load_bin(p, device=device)
+    raise GraphFormatError(f"unknown graph extension {p.suffix!r}", p)
 
 
 ADJ_HEADER = b"AdjacencyGraph"

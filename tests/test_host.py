@@ -96,6 +96,21 @@ def test_workspace_is_linear_in_n(lib):
         assert extra <= 4 * (m // 256 + 2) + 8 * (m // 2048 + 2) + 4096
 
 
+def test_workspace_non_decreasing_in_n(lib):
+    """the list-ranking ruler spacing coarsens with n (2^18, 2^25, 2^28), so the
+    ruler arrays are sized for the largest count any smaller graph needs -- a workspace
+    sized for the largest graph of a batch must fit every smaller one."""
+    prev = 0
+    pts = []
+    for t in (1 << 18, 1 << 25, 1 << 28):
+        pts += [t - 2, t - 1, t, t + 1]
+    pts += [1, 2, 1000, (1 << 20) + 3, (1 << 30)]
+    for n in sorted(pts):
+        b = lib.pasgal_bcc_workspace_bytes(n, 0)
+        assert b >= prev, n
+        prev = b
+
+
 def test_validate_workspace_is_linear_in_m(lib):
     """Validation scratch: one 8-byte key per run of up slots (<= m/2) plus per-CTA
     histograms; an undersized workspace is refused before any device work."""

@@ -90,3 +90,42 @@ def test_e2e_participants_agree_across_ranks():
     assert [r[1] for r in res] == [2, 2]
     assert [r[2] for r in res] == [0, 0]
     assert res[0][3] == res[1][3] == [2.0, 0.0]
+
+
+def _bench_json(args, env_extra=None):
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), *args], capture_output=True, text=True,
+                       env=env, timeout=150)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.timeout(180)
+def test_bench_gpus_2_spawns_two_ranks():
+    """`python bench.py --gpus 2` outside torchrun launches two ranks itself (the driver's
+    command form); each rank gets its own replica seed and its own c5b instances."""
+    d = _bench_json(["--gpus", "2", "--dry-run"])
+    assert d["n_gpus"] == 2 and d["gpus_arg"] == 2
+    seeds = [r[1] for r in d["ranks"]]
+    assert sorted(r[0] for r in d["ranks"]) == [0, 1] and len(set(seeds)) == 2
+    d = _bench_json(["--gpus", "2", "--dry-run", "--config", "c5b"])
+    assert sum(r[2] for r in d["ranks"]) == 64 and sum(r[3] for r in d["ranks"]) == sum(range(64))
+
+
+def test_bench_rejects_world_mismatch():
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
