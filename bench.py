@@ -768,6 +768,25 @@ def run_e2e(args, off_h, tgt_h, dev, n, m, participate=True, k=1, world=1):
     if world > 1:
         out["ranks"] = k
         out["bytes_per_step_note"] = "h2d/d2h bytes are per participating rank"
+    # vertex mode: the same call returning the reference's O(n) parallel-mode BccLabels
+    # (comp/parent/first, results.py:49-52): no per-slot labelling pass, 13 B/vertex back
+    vdt = 0.0
+    if participate:
+        hbv = pg.HostBuffers.allocate(n, m, edge_labels=False)
+        res = pg.bcc(g, device=dev, host_out=hbv, edge_labels=False)     # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = pg.bcc(g, device=dev, host_out=hbv, edge_labels=False)
+        vdt = (time.perf_counter() - t0) / steps
+        del res, hbv
+    _sync()
+    vdt, = _allreduce([vdt], dist.ReduceOp.MAX, dev) if world > 1 else [vdt]
+    out["vertex_mode"] = {"value": edges / vdt, "unit": UNIT, "ms_per_step": vdt * 1e3, "steps": steps,
+                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 13 * n + 8,
+                          "path": "paper_2404_17101_b200.bcc(g, edge_labels=False): H2D, validate, FAST-BCC "
+                                  "without the per-slot pass, D2H articulation bytes + comp/parent/first + count "
+                                  "(the reference's O(n) BccLabels mode, results.py:49-52)"}
     # pipelined: the same per-step copies and work, consecutive steps overlapped
     pg.release_workspace()
     torch.cuda.empty_cache()

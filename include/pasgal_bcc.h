@@ -61,7 +61,11 @@ typedef struct {
  *   bcc_count   int64 scalar (device).
  *   comp/parent/first  optional uint32[n] (NULL to skip): the parallel-mode fields of
  *               BccLabels (results.py:76-88): skeleton component, spanning-forest parent
- *               (self for roots), preorder rank. */
+ *               (self for roots), preorder rank.
+ *   Vertex mode: edge_label may be NULL when comp, parent and first are all given (and
+ *   CANONICAL is not set).  The per-slot labelling pass is then skipped and the result is
+ *   the O(n) parallel-mode BccLabels ("keeps the result O(n) sized", results.py:49-52):
+ *   label(u,w) = comp of the endpoint with the larger first (results.py:80-87). */
 typedef struct {
     uint32_t* edge_label;
     uint32_t* artic_bits;
@@ -262,6 +266,13 @@ int pasgal_msbfs_ex(const pasgal_csr_t* g, const int64_t* sources, int nsources,
  * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.
  * Asynchronous on `stream`. */
 int pasgal_bits_to_bytes(const uint32_t* bits, int64_t n, uint8_t* bytes, void* stream);
+
+/* Run checksum of a canonical labelling, the device twin of
+ * results.canonical_checksum: out[0] = sum over slots s of labels[s] * w(s) mod 2^64 with
+ * w(s) = ((s * 0x9E3779B1) mod 2^32) | 1, out[1] = number of set articulation bits.  `out`
+ * is DEVICE uint64[2]; bcc_count completes the triple.  Asynchronous. */
+int pasgal_canonical_checksum(const uint32_t* labels, int64_t m_slots, const uint32_t* artic_bits, int64_t n,
+                              uint64_t* out, void* stream);
 
 const char* pasgal_strerror(int status);
 

@@ -134,12 +134,14 @@ def validate_device(offsets, targets, workspace=None):
 
 
 def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out=None,
-               workspace=None, forest=False, events=None, _defer_validation=False):
+               workspace=None, forest=False, edge_labels=True, events=None, _defer_validation=False):
     """FAST-BCC on a device CSR (offsets int64[n+1], targets int32[M], both CUDA).
 
     Returns ``DeviceBcc``.  ``canonical=True`` labels every edge with the minimum
     undirected edge id of its BCC.  ``forest=True`` also returns comp/parent/first (the
-    parallel-mode fields of BccLabels).  ``events``: optional list of
+    parallel-mode fields of BccLabels).  ``edge_labels=False`` (vertex mode, implies
+    ``forest``) skips the per-slot labelling pass: the result is O(n) sized
+    (results.py:49-52) and ``edge_label`` is None.  ``events``: optional list of
     ``torch.cuda.Event(enable_timing=True)`` (one per stage, ``_lib.STAGES``) recorded at
     the stage boundaries on the current stream."""
     lib = _lib.load()
@@ -155,12 +157,16 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
     ws = workspace if workspace is not None else _workspace(dev, need)
     if ws.numel() < need:
         raise ValueError("workspace too small")
+    if not edge_labels:
+        if canonical:
+            raise ValueError("canonical labels need edge_labels=True")
+        forest = True
     # validation is split: its streaming half gates the call, its symmetry half runs after
     # the BCC kernels on a side stream (overlapping the caller's next copies when deferred)
     pending = _validate_begin(offsets, targets) if validate else None
     if out is None:
         out = DeviceBcc(
-            edge_label=torch.empty(m, dtype=torch.int32, device=dev),
+            edge_label=torch.empty(m, dtype=torch.int32, device=dev) if edge_labels else None,
             artic_bits=torch.empty((n + 31) // 32, dtype=torch.int32, device=dev),
             bcc_count=torch.empty(1, dtype=torch.int64, device=dev),
         )
@@ -169,7 +175,9 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
             out.parent = torch.empty(n, dtype=torch.int32, device=dev)
             out.first = torch.empty(n, dtype=torch.int32, device=dev)
     csr = _csr_struct(offsets, targets)
-    o = _lib.PasgalBccOut(out.edge_label.data_ptr() if m else 0, out.artic_bits.data_ptr() if n else 0,
+    if not edge_labels and (out.comp is None or out.parent is None or out.first is None):
+        raise ValueError("vertex mode needs out.comp, out.parent and out.first")
+    o = _lib.PasgalBccOut(out.edge_label.data_ptr() if (m and edge_labels and out.edge_label is not None) else 0, out.artic_bits.data_ptr() if n else 0,
                           out.bcc_count.data_ptr(),
                           out.comp.data_ptr() if out.comp is not None else 0,
                           out.parent.data_ptr() if out.parent is not None else 0,
@@ -253,20 +261,19 @@ def canonicalize_device(offsets, targets, labels, label_bound=None):
 
 
 def canonical_checksum_device(canon_labels, artic_bits, bcc_count):
-    """Device twin of results.canonical_checksum: canon_labels is the int32 storage of the
-    canonical uint32 labels (bcc_device(..., canonical=True).edge_label), artic_bits the
-    device bitmap, bcc_count the device count.  Integer products and sums wrap mod 2^64 on
-    the device exactly as in the host's uint64 arithmetic."""
+    """Device twin of results.canonical_checksum (pasgal_canonical_checksum: one pass, no
+    M-sized temporaries): canon_labels is the int32 storage of the canonical uint32 labels
+    (bcc_device(..., canonical=True).edge_label), artic_bits the device bitmap, bcc_count
+    the device count.  Products and sums wrap mod 2^64 exactly as the host's uint64 ones."""
     m = canon_labels.shape[0]
-    lab = canon_labels.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    s = torch.arange(m, dtype=torch.int64, device=canon_labels.device)
-    w = ((s * 0x9E3779B1) & 0xFFFFFFFF) | 1
-    h = int((lab * w).sum().item()) % (1 << 64) if m else 0
-    bits = artic_bits.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    nart = 0
-    for k in range(32):                      # popcount over the bitmap words
-        nart += int(((bits >> k) & 1).sum().item())
-    return int(bcc_count.item()), nart, h
+    nw = artic_bits.shape[0]
+    out = torch.empty(2, dtype=torch.int64, device=canon_labels.device)
+    st = _lib.load().pasgal_canonical_checksum(_vp(canon_labels.contiguous()), int(m), _vp(artic_bits.contiguous()),
+                                                int(32 * nw), _vp(out),
+                                                ctypes.c_void_p(torch.cuda.current_stream(canon_labels.device).cuda_stream))
+    _lib.check(st, "checksum")
+    h, nart = (int(x) for x in out.cpu().tolist())
+    return int(bcc_count.item()), nart, h % (1 << 64)
 
 
 def same_partition_device(offsets, targets, labels_a, labels_b, label_bound=None):
@@ -297,16 +304,24 @@ class HostBuffers:
     labels and articulation flags are copied straight into them and the returned
     BccLabels views them (no host-side copy or unpack)."""
 
-    edge_label: torch.Tensor    # int32 [>= M], cpu (pinned)
+    edge_label: torch.Tensor    # int32 [>= M], cpu (pinned); None in vertex mode
     articulation: torch.Tensor  # uint8 [>= n], cpu (pinned)
+    comp: torch.Tensor = None   # int32 [>= n] each, vertex mode (edge_labels=False)
+    parent: torch.Tensor = None
+    first: torch.Tensor = None
 
     @staticmethod
-    def allocate(n, m, pinned=True):
-        return HostBuffers(torch.empty(max(m, 1), dtype=torch.int32, pin_memory=pinned),
-                           torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=pinned))
+    def allocate(n, m, pinned=True, edge_labels=True):
+        def buf(k, dt):
+            return torch.empty(max(k, 1), dtype=dt, pin_memory=pinned)
+
+        if edge_labels:
+            return HostBuffers(buf(m, torch.int32), buf(n, torch.uint8))
+        return HostBuffers(None, buf(n, torch.uint8), buf(n, torch.int32), buf(n, torch.int32), buf(n, torch.int32))
 
 
-def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False, host_out=None):
+def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=False, host_out=None,
+        edge_labels=True):
     """Drop-in for ``bcc_hopcroft_tarjan(g)``: biconnected components of a symmetric graph.
 
     ``g`` is any object with ``offsets`` (int64[n+1]) and ``targets`` (uint32/int32/int64
@@ -314,6 +329,11 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
     the device, validated there (``ValueError("biconnectivity requires a symmetric graph")``
     as in oracles.py:127-128), processed, and the labels, articulation flags and count are
     copied back into a ``BccLabels``.  Rows must be sorted (every reference builder sorts).
+
+    ``edge_labels=False`` returns the reference's O(n) parallel-mode ``BccLabels``
+    (comp/parent/first, results.py:49-52, 76-88) instead of per-slot labels: the device
+    skips the labelling pass and the copy back is 13 bytes per vertex instead of 4 per slot;
+    ``edge_labels(g)`` derives the per-slot labels on the host on demand.
 
     The work runs on a high-priority stream: the validation's symmetry check, on the
     lowest-priority side stream, then only fills the SMs the BCC kernels leave idle
@@ -326,7 +346,7 @@ def bcc(g, *, seed=0, validate=True, canonical=False, device="cuda", forest=Fals
     hp = _priority_stream(dev)
     hp.wait_stream(cur)
     with torch.cuda.stream(hp):
-        res = _bcc_host(g, seed, validate, canonical, device, forest, host_out)
+        res = _bcc_host(g, seed, validate, canonical, device, forest, host_out, edge_labels)
     cur.wait_stream(hp)
     return res
 
@@ -341,7 +361,7 @@ def _priority_stream(device):
     return _priority_streams[device]
 
 
-def _bcc_host(g, seed, validate, canonical, device, forest, host_out):
+def _bcc_host(g, seed, validate, canonical, device, forest, host_out, edge_labels=True):
     if isinstance(g, DeviceGraph):
         off_d, tgt_d = g.offsets, g.targets
     else:
@@ -362,13 +382,25 @@ def _bcc_host(g, seed, validate, canonical, device, forest, host_out):
     n = off_d.shape[0] - 1
     m = tgt_d.shape[0]
     r = bcc_device(off_d, tgt_d, seed=seed, validate=validate, canonical=canonical, forest=forest,
-                   _defer_validation=validate)
+                   edge_labels=edge_labels, _defer_validation=validate)
     pending = None
     if validate:
         r, pending = r
     art_d = articulation_bytes_device(r.artic_bits, n)
     done = torch.cuda.Event()
     done.record()                           # BCC kernels + articulation bytes
+    if not edge_labels:
+        hb = host_out if host_out is not None else HostBuffers.allocate(n, m, edge_labels=False)
+        fields = []
+        for src, dst in ((art_d, hb.articulation), (r.comp, hb.comp), (r.parent, hb.parent), (r.first, hb.first)):
+            dst[:n].copy_(src[:n], non_blocking=True)
+            fields.append(dst[:n].numpy())
+        if pending is not None:
+            pending.finish(after=done)
+        count = int(r.bcc_count.item())     # synchronises the stream
+        art, comp, par, fst = fields
+        return BccLabels(art.view(np.bool_), count, comp=comp.view(np.uint32), parent=par.view(np.uint32),
+                         first=fst.view(np.uint32))
     if host_out is not None:
         host_out.edge_label[:m].copy_(r.edge_label, non_blocking=True)
         host_out.articulation[:n].copy_(art_d, non_blocking=True)

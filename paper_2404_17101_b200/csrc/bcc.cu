@@ -1631,7 +1631,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (w.nch > 0) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, w.GBIT, w.ctr,
+    if (w.nch > 0 && out->edge_label) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, w.GBIT, w.ctr,
                                                                           out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
@@ -1812,6 +1812,38 @@ int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st) {
     if (n <= 0) return PASGAL_OK;
     const i64 words = cdiv(n, 32);
     k_bits_to_bytes<<<nblk(words, 256), 256, 0, st>>>(bits, n, out);
+    PG_LAUNCH_CHECK();
+    return PASGAL_OK;
+}
+
+// Run checksum (results.canonical_checksum's device twin): out[0] += sum over slots of
+// lab[s] * (((s * 0x9E3779B1) mod 2^32) | 1) mod 2^64 (unsigned wraparound), out[1] += the
+// articulation popcount.  One grid-stride pass, a warp reduction and one atomic per warp.
+__global__ void k_checksum(const u32* __restrict__ lab, i64 m, const u32* __restrict__ bits, i64 nw,
+                           unsigned long long* out) {
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    u64 h = 0, c = 0;
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += stride)
+        h += (u64)__ldcs(lab + s) * (u64)((u32)((u64)s * 0x9E3779B1ull) | 1u);
+    for (i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x; k < nw; k += stride) c += __popc(bits[k]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+        c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (h) atomicAdd(out, (unsigned long long)h);
+        if (c) atomicAdd(out + 1, (unsigned long long)c);
+    }
+}
+
+int canonical_checksum(const u32* lab, i64 m, const u32* bits, i64 n, unsigned long long* out, cudaStream_t st) {
+    PG_CUDA_TRY(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st));
+    const i64 work = m > cdiv(n, 32) ? m : cdiv(n, 32);
+    if (work <= 0) return PASGAL_OK;
+    i64 blocks = cdiv(work, 256 * 8);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_checksum<<<(unsigned)blocks, 256, 0, st>>>(lab, m, bits, cdiv(n, 32), out);
     PG_LAUNCH_CHECK();
     return PASGAL_OK;
 }

@@ -21,6 +21,8 @@ size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
 int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
                         cudaStream_t st);
 int csr_first_error(const pasgal_csr_t* g, void* scratch, int64_t* host_out, cudaStream_t st);
+int canonical_checksum(const uint32_t* lab, int64_t m, const uint32_t* bits, int64_t n, unsigned long long* out,
+                       cudaStream_t st);
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
               cudaStream_t st);
 int csr_validate(const pasgal_csr_t* g, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -61,7 +63,11 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
                   uint64_t seed, uint32_t flags, void* stream, pasgal_bcc_prof_t* prof) {
     int s = check_csr(g);
     if (s) return s;
-    if (!out || !out->bcc_count || (g->n > 0 && !out->artic_bits) || (g->m_slots > 0 && !out->edge_label))
+    if (!out || !out->bcc_count || (g->n > 0 && !out->artic_bits)) return PASGAL_EINVAL;
+    // vertex mode (edge_label NULL): the O(n) parallel-mode fields replace the per-slot labels
+    const bool vertex_mode = !out->edge_label;
+    if (g->m_slots > 0 && vertex_mode &&
+        ((flags & PASGAL_BCC_CANONICAL) || (g->n > 0 && (!out->comp || !out->parent || !out->first))))
         return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
     return pg::bcc_launch(g, out, workspace, workspace_bytes, seed, flags, (cudaStream_t)stream, prof);
@@ -222,6 +228,12 @@ int pasgal_adj_parse(const uint8_t* text, int64_t nbytes, void* temp, size_t tem
     if (!temp) return PASGAL_EWORKSPACE;
     return pg::adj_parse(text, nbytes, temp, temp_bytes, n, m, weighted, offsets, targets, first_err, uncertain,
                          n_uncertain, (cudaStream_t)stream);
+}
+
+int pasgal_canonical_checksum(const uint32_t* labels, int64_t m_slots, const uint32_t* artic_bits, int64_t n,
+                              uint64_t* out, void* stream) {
+    if (n < 0 || m_slots < 0 || !out || (m_slots > 0 && !labels) || (n > 0 && !artic_bits)) return PASGAL_EINVAL;
+    return pg::canonical_checksum(labels, m_slots, artic_bits, n, (unsigned long long*)out, (cudaStream_t)stream);
 }
 
 int pasgal_bits_to_bytes(const uint32_t* bits, int64_t n, uint8_t* bytes, void* stream) {

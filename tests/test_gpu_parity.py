@@ -106,6 +106,37 @@ def test_forest_outputs_reproduce_labels_by_reference_rule():
                 assert first[p] < first[v]
 
 
+def test_vertex_mode_output_matches_reference_partition():
+    """bcc(g, edge_labels=False): the O(n) parallel-mode BccLabels (results.py:49-52, 76-88),
+    no per-slot labels on the device or the host until edge_labels(g) derives them; the
+    reference's comparator sees the same partition, articulation and count as the golden
+    reference outputs, through both the package's and the reference's own edge rule."""
+    for fname in ["c1_grid256_p06_s1.npz", "knn_13_k5_seed3.npz", "rmat_s12_d16_seed7.npz"]:
+        case = golden_io.single(fname)
+        g = pg.Graph(case.offsets, case.targets)
+        res = pg.bcc(g, edge_labels=False)
+        assert res.raw_edge_label is None
+        assert res.bcc_count == case.count
+        assert np.array_equal(res.articulation, case.articulation)
+        assert np.array_equal(pg.canonical_edge_partition(g, res), case.canon)
+        # the reference's own rule (tree edge -> child's comp, else larger-first endpoint)
+        comp, parent, first = (np.asarray(x, dtype=np.int64) for x in (res._comp, res._parent, res._first))
+        src = np.repeat(np.arange(case.n, dtype=np.int64), np.diff(case.offsets))
+        dst = case.targets.astype(np.int64)
+        lab = np.where(parent[dst] == src, comp[dst], np.where(parent[src] == dst, comp[src], -1))
+        rest = lab == -1
+        lab[rest] = np.where(first[src[rest]] > first[dst[rest]], comp[src[rest]], comp[dst[rest]])
+        keep = src < dst
+        assert np.array_equal(pg.canonical_relabel(lab[keep]), case.canon)
+    # pinned host buffers are filled in place
+    case = golden_io.single("c1_grid256_p06_s1.npz")
+    hb = pg.HostBuffers.allocate(case.n, case.m, edge_labels=False)
+    res = pg.bcc(pg.Graph(case.offsets, case.targets), edge_labels=False, host_out=hb)
+    assert res._comp.ctypes.data == hb.comp.data_ptr()
+    with pytest.raises(ValueError):
+        pg.bcc(pg.Graph(case.offsets, case.targets), edge_labels=False, canonical=True)
+
+
 def test_validation_errors_match_reference():
     # non-symmetric (oracles.py:127-128)
     off = np.array([0, 1, 1, 1], dtype=np.int64)
