@@ -112,6 +112,17 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
                   size_t workspace_bytes, uint64_t seed, uint32_t flags, void* stream,
                   pasgal_bcc_prof_t* prof);
 
+/* CUDA-graph form of pasgal_bcc for repeated calls on fixed buffers (small graphs are
+ * launch-bound): _create captures one call's launches for these pointers, sizes, seed and
+ * flags (nothing runs); _launch replays it on `stream` -- exactly a pasgal_bcc call on
+ * whatever the buffers hold then -- and reports the kernel launches it contains;
+ * _destroy frees it.  The buffers must stay allocated while the graph is used. */
+typedef struct pasgal_bcc_graph_s* pasgal_bcc_graph_t;
+int pasgal_bcc_graph_create(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace,
+                            size_t workspace_bytes, uint64_t seed, uint32_t flags, pasgal_bcc_graph_t* graph);
+int pasgal_bcc_graph_launch(pasgal_bcc_graph_t graph, void* stream, int* launches);
+void pasgal_bcc_graph_destroy(pasgal_bcc_graph_t graph);
+
 /* Device validation of the BCC preconditions (graph.py:87-96, 123-158):
  * offsets monotone from 0 to m_slots, targets in [0,n), rows sorted (non-decreasing), and
  * the slot multiset closed under reversal (the k-th copy of w in row u has a k-th copy of

@@ -57,6 +57,10 @@ SIGNATURES = {
     "pasgal_bcc": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP]),
     "pasgal_bcc_ex": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP,
                              ctypes.POINTER(PasgalBccProf)]),
+    "pasgal_bcc_graph_create": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32,
+                                       ctypes.POINTER(ctypes.c_void_p)]),
+    "pasgal_bcc_graph_launch": (_INT, [_VP, _VP, ctypes.POINTER(ctypes.c_int)]),
+    "pasgal_bcc_graph_destroy": (None, [_VP]),
     "pasgal_cc": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _VP, _VP, _SZ, _U64, _VP]),
     "pasgal_canonicalize_temp_bytes": (_SZ, [_I64, _I64, _I64]),
     "pasgal_canonicalize": (_INT, [ctypes.POINTER(PasgalCsr), _VP, _I64, _VP, _VP, _SZ, _VP]),

@@ -48,6 +48,7 @@ def _workspace(device, nbytes, kind="bcc"):
 
 
 def release_workspace():
+    _graphs.clear()
     _ws_cache.clear()
     _side_streams.clear()
     _priority_streams.clear()
@@ -133,8 +134,40 @@ def validate_device(offsets, targets, workspace=None):
     _lib.check(st, "validate")
 
 
+GRAPH_MAX_N = 1 << 22       # auto CUDA-graph replay below this size (launch-bound calls)
+_GRAPH_CACHE_SIZE = 8
+
+
+class _GraphCache:
+    """Captured pasgal_bcc calls (pasgal_bcc_graph_create), keyed by every pointer, size,
+    seed and flag they were captured with, least recently used evicted first."""
+
+    def __init__(self):
+        self.entries = {}
+
+    def get(self, key, create):
+        h = self.entries.pop(key, None)
+        if h is None:
+            h = create()
+            while len(self.entries) >= _GRAPH_CACHE_SIZE:
+                old = next(iter(self.entries))
+                _lib.load().pasgal_bcc_graph_destroy(self.entries.pop(old))
+        self.entries[key] = h
+        return h
+
+    def clear(self):
+        lib = _lib.load() if self.entries else None
+        for h in self.entries.values():
+            lib.pasgal_bcc_graph_destroy(h)
+        self.entries.clear()
+
+
+_graphs = _GraphCache()
+
+
 def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out=None,
-               workspace=None, forest=False, edge_labels=True, events=None, _defer_validation=False):
+               workspace=None, forest=False, edge_labels=True, events=None, graph=None,
+               _defer_validation=False):
     """FAST-BCC on a device CSR (offsets int64[n+1], targets int32[M], both CUDA).
 
     Returns ``DeviceBcc``.  ``canonical=True`` labels every edge with the minimum
@@ -143,7 +176,10 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
     ``forest``) skips the per-slot labelling pass: the result is O(n) sized
     (results.py:49-52) and ``edge_label`` is None.  ``events``: optional list of
     ``torch.cuda.Event(enable_timing=True)`` (one per stage, ``_lib.STAGES``) recorded at
-    the stage boundaries on the current stream."""
+    the stage boundaries on the current stream.  ``graph``: replay a captured CUDA graph of
+    the call (pasgal_bcc_graph_*; cached per pointer/size/seed/flags set).  The default
+    (None) does so for graphs below GRAPH_MAX_N vertices when the caller passes both
+    ``out`` and ``workspace`` (fixed buffers: a repeated call), without ``events``."""
     lib = _lib.load()
     if offsets.device.type != "cuda" or targets.device.type != "cuda":
         raise ValueError("bcc_device needs CUDA tensors")
@@ -193,8 +229,25 @@ def bcc_device(offsets, targets, *, seed=0, validate=False, canonical=False, out
             handles.append(e.cuda_event)
         arr = (ctypes.c_void_p * len(handles))(*handles)
         prof = _lib.PasgalBccProf(ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), len(handles), 0)
-    st = lib.pasgal_bcc_ex(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
-                           flags, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prof))
+    if graph is None:
+        graph = events is None and workspace is not None and out is not None and n < GRAPH_MAX_N
+    if graph and events is None:
+        key = (dev, offsets.data_ptr(), targets.data_ptr(), n, m, o.edge_label, o.artic_bits, o.bcc_count, o.comp,
+               o.parent, o.first, ws.data_ptr(), ws.numel(), int(seed) & (2**64 - 1), flags)
+
+        def create():
+            h = ctypes.c_void_p()
+            _lib.check(lib.pasgal_bcc_graph_create(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(),
+                                                   int(seed) & (2**64 - 1), flags, ctypes.byref(h)), "bcc graph")
+            return h
+
+        nl = ctypes.c_int(0)
+        st = lib.pasgal_bcc_graph_launch(_graphs.get(key, create), ctypes.c_void_p(stream.cuda_stream),
+                                         ctypes.byref(nl))
+        prof.launches = nl.value
+    else:
+        st = lib.pasgal_bcc_ex(ctypes.byref(csr), ctypes.byref(o), _vp(ws), ws.numel(), int(seed) & (2**64 - 1),
+                               flags, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prof))
     if st != 0 and pending is not None:
         pending.finish()            # a symmetry error explains a failure better
     _lib.check(st, "bcc")

@@ -192,6 +192,17 @@ __global__ void k_canon_init(i64 n, u32* UCNT, i64 nlab, u32* CANON) {
 constexpr int LOCAL_LB = PG_LOCAL_LB;
 constexpr int LOCAL_B = 1 << LOCAL_LB;
 constexpr int LOCAL_T = 512;
+// Block size 2^lb: LOCAL_B ids unless that leaves the GPU idle -- small graphs (C1: 8 CTAs
+// of 8192 ids on 148 SMs) take smaller blocks so at least ~2 CTAs per SM run.
+// PASGAL_BCC_LOCAL_LB overrides it (sweeps).
+static inline int local_lb(i64 n) {
+    const char* e = getenv("PASGAL_BCC_LOCAL_LB");
+    const int v = e ? atoi(e) : 0;
+    if (v >= 6 && v <= LOCAL_LB) return v;
+    int lb = LOCAL_LB;
+    while (lb > 9 && cdiv(n, (i64)1 << lb) < 2 * 148) --lb;
+    return lb;
+}
 
 __device__ __forceinline__ u32 sfind(volatile u32* sp, u32 x) {
     for (;;) {
@@ -221,12 +232,12 @@ __device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
 // It also writes the warp-chunk row partition: CROW[c] = the nonempty row holding slot
 // c * WCH, from the row's own offsets (no per-chunk binary search; a hub row writes the
 // entries of all the chunks that start inside it).
-__global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restrict__ off,
+__global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, int lb, const i64* __restrict__ off,
                                                       const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
                                                       u32* HEAD, u32* CROW) {
     __shared__ u32 sp[LOCAL_B];
-    const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
-    const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
+    const i64 b0 = (i64)blockIdx.x << lb;
+    const int cnt = (int)(n - b0 < (1 << lb) ? n - b0 : (1 << lb));
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
         sp[i] = (u32)i;
         reinterpret_cast<uint4*>(HAB)[b0 + i] = make_uint4(PG_INV, PG_INV, 0u, 0u);   // whole 16-byte record
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, const i64* __restri
             for (i64 c = cdiv(a, WCH); c * WCH < b; ++c) CROW[c] = (u32)v;
         for (int k = 0; k < NSAMPLE && a + k < b; ++k) {
             i64 w = tgt[a + k];
-            if ((w >> LOCAL_LB) != blockIdx.x) continue;
+            if ((w >> lb) != blockIdx.x) continue;
             u32 hi = slink(sp, (u32)i, (u32)(w - b0));
             if (hi != PG_INV) HAB[2 * (b0 + hi)] = make_uint2((u32)v, (u32)w);
         }
@@ -275,7 +286,8 @@ __device__ __forceinline__ void uf_find_lockstep(u32* P, u32 (&x)[K]) {
     }
 }
 
-__global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
+__global__ void k_cc_sample(i64 n, int lb, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
+                            uint2* HAB) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     i64 a = off[v], b = off[v + 1];
@@ -286,7 +298,7 @@ __global__ void k_cc_sample(i64 n, const i64* __restrict__ off, const int32_t* _
     for (int k = 0; k < NSAMPLE; ++k) {
         act[k] = a + k < b;
         t[k] = act[k] ? (u32)tgt[a + k] : (u32)v;
-        act[k] = act[k] && (t[k] >> LOCAL_LB) != (u32)(v >> LOCAL_LB);
+        act[k] = act[k] && (t[k] >> lb) != (u32)(v >> lb);
         x[k + 1] = act[k] ? t[k] : (u32)v;
         any |= act[k];
     }
@@ -370,20 +382,33 @@ __global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i
     compress_ilp<ILP>(n, P, root, idx);
 }
 
-// most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root)
+// most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root).  Counts in
+// a shared-memory open-addressing table (one insert per thread) instead of every thread
+// scanning all samples (O(S^2) shared loads: 24 us per call, a visible share at C1).
+constexpr int GIANT_HASH = 2 * GIANT_SAMPLES;
 __global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u64 seed, u32* out) {
-    __shared__ u32 s[GIANT_SAMPLES];
+    __shared__ u32 hk[GIANT_HASH], hc[GIANT_HASH];
     typedef cub::BlockReduce<u64, GIANT_SAMPLES> BR;
     __shared__ typename BR::TempStorage tmp;
-    int t = threadIdx.x;
-    u32 v = (u32)(draw(seed ^ 0x5EEDB1CCull, (u64)t) % (u64)n);
-    u32 r = ldcg(P + v);
-    s[t] = r;
+    const int t = threadIdx.x;
+    for (int k = t; k < GIANT_HASH; k += GIANT_SAMPLES) {
+        hk[k] = PG_INV;
+        hc[k] = 0;
+    }
+    const u32 v = (u32)(draw(seed ^ 0x5EEDB1CCull, (u64)t) % (u64)n);
+    const u32 r = ldcg(P + v);
     __syncthreads();
-    u32 cnt = 0;
-    for (int k = 0; k < GIANT_SAMPLES; ++k) cnt += s[k] == r;
-    u64 key = ((u64)cnt << 32) | (u64)(PG_INV - r);
-    u64 best = BR(tmp).Reduce(key, cub::Max());
+    u32 h = (r * 0x9E3779B1u) >> (32 - 11);      // GIANT_HASH = 2^11 slots
+    for (;;) {
+        const u32 k = atomicCAS(hk + h, PG_INV, r);
+        if (k == PG_INV || k == r) break;
+        h = (h + 1) & (GIANT_HASH - 1);
+    }
+    atomicAdd(hc + h, 1u);
+    __syncthreads();
+    const u32 cnt = hc[h];
+    const u64 key = ((u64)cnt << 32) | (u64)(PG_INV - r);
+    const u64 best = BR(tmp).Reduce(key, cub::Max());
     if (t == 0) *out = PG_INV - (u32)(best & 0xFFFFFFFFu);
 }
 
@@ -648,6 +673,49 @@ __global__ void k_wyllie(i64 ns, const u32* __restrict__ len_in, const u32* __re
     nxt_out[s] = nx;
 }
 
+// All Wyllie rounds in one CTA when the rulers fit in shared memory (small graphs: C1 has
+// 16K rulers and took 15 launches): SPLEN/SPNEXT[0] in, SPLEN[1] out.
+constexpr int WY_T = 1024, WY_IPT = 20, WY_MAX = WY_T * WY_IPT;
+__global__ void __launch_bounds__(WY_T) k_wyllie_small(i64 ns, const u32* __restrict__ len_in,
+                                                       const u32* __restrict__ nxt_in, u32* len_out) {
+    extern __shared__ u32 wy[];
+    u32* L = wy;
+    u32* X = wy + WY_MAX;
+    for (i64 s = threadIdx.x; s < ns; s += WY_T) {
+        L[s] = len_in[s];
+        X[s] = nxt_in[s];
+    }
+    __syncthreads();
+    for (;;) {
+        u32 l[WY_IPT], x[WY_IPT];
+        int live = 0;
+#pragma unroll
+        for (int j = 0; j < WY_IPT; ++j) {
+            const i64 s = threadIdx.x + (i64)j * WY_T;
+            if (s < ns) {
+                l[j] = L[s];
+                x[j] = X[s];
+                if (x[j] != PG_INV) {
+                    l[j] += L[x[j]];
+                    x[j] = X[x[j]];
+                    live |= x[j] != PG_INV;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < WY_IPT; ++j) {
+            const i64 s = threadIdx.x + (i64)j * WY_T;
+            if (s < ns) {
+                L[s] = l[j];
+                X[s] = x[j];
+            }
+        }
+        if (!__syncthreads_or(live)) break;
+    }
+    for (i64 s = threadIdx.x; s < ns; s += WY_T) len_out[s] = L[s];
+}
+
 constexpr int LR_T = 256;
 
 __global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, u32 lrs, const u32* __restrict__ NEXT,
@@ -906,6 +974,22 @@ __global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i
     dst[b] = v;
 }
 
+// every level of the sparse table in one CTA (small graphs: 11-15 launches otherwise)
+constexpr i64 RMQ_SMALL = 1 << 16;
+__global__ void __launch_bounds__(1024) k_rmq_levels_small(i64 nb, i64 lv, uint2* ST) {
+    for (i64 k = 1; k < lv; ++k) {
+        const uint2* src = ST + (k - 1) * nb;
+        uint2* dst = ST + k * nb;
+        const i64 half = (i64)1 << (k - 1);
+        for (i64 b = threadIdx.x; b < nb; b += blockDim.x) {
+            uint2 v = src[b];
+            if (b + half < nb) v = mm(v, src[b + half]);
+            dst[b] = v;
+        }
+        __syncthreads();
+    }
+}
+
 // low/high of every preorder position, fence test, and Last-CC union of the non-fence
 // tree edges (S5 fused).
 __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E,
@@ -989,18 +1073,18 @@ __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
 // Last-CC local phase over preorder positions: non-fence tree edges (i, parent position)
 // inside a block of LOCAL_B positions are joined in shared memory (a child's parent is
 // usually a few positions back), then C[i] = block root is published.
-__global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restrict__ FPF, const uint2* __restrict__ W,
-                                                       const u32* __restrict__ E, u32* C) {
+__global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, int lb, const u32* __restrict__ FPF,
+                                                       const uint2* __restrict__ W, const u32* __restrict__ E, u32* C) {
     __shared__ u32 sp[LOCAL_B];
-    const i64 b0 = (i64)blockIdx.x << LOCAL_LB;
-    const int cnt = (int)(n - b0 < LOCAL_B ? n - b0 : LOCAL_B);
+    const i64 b0 = (i64)blockIdx.x << lb;
+    const int cnt = (int)(n - b0 < (1 << lb) ? n - b0 : (1 << lb));
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) sp[i] = (u32)i;
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
         u32 f = FPF[b0 + i];
         {     // the high tag's cross edge (k_cc2_links), when it stays in the block
             const u32 hi = __ldcs(&W[b0 + i].y);
-            if (hi > __ldcs(E + b0 + i) && (i64)hi < b0 + LOCAL_B) slink(sp, (u32)i, (u32)(hi - b0));
+            if (hi > __ldcs(E + b0 + i) && (i64)hi < b0 + (1 << lb)) slink(sp, (u32)i, (u32)(hi - b0));
         }
         if (f & 0x80000000u) continue;     // fence, or a root (PG_INV)
         if ((i64)f >= b0) slink(sp, (u32)i, (u32)(f - b0));
@@ -1018,15 +1102,15 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, const u32* __restr
 // Both block-crossing global links of a position in one pass: its non-fence tree edge and
 // the cross edge of its high tag (a cross edge never points into its own subtree, so
 // hi > last >= i and a block-local one was taken by k_cc2_local).
-__global__ void k_cc2_links(i64 n, const u32* __restrict__ FPF, const uint2* __restrict__ W,
+__global__ void k_cc2_links(i64 n, int lb, const u32* __restrict__ FPF, const uint2* __restrict__ W,
                             const u32* __restrict__ E, u32* C) {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const u32 f = FPF[i];
     const u32 hi = __ldcs(&W[i].y);
     const u32 e = __ldcs(E + i);
-    const bool tree = !(f & 0x80000000u) && (f >> LOCAL_LB) != (u32)(i >> LOCAL_LB);
-    const bool cross = hi > e && (hi >> LOCAL_LB) != (u32)(i >> LOCAL_LB);
+    const bool tree = !(f & 0x80000000u) && (f >> lb) != (u32)(i >> lb);
+    const bool cross = hi > e && (hi >> lb) != (u32)(i >> lb);
     if (tree) uf_link(C, (u32)i, f);
     if (cross) uf_link(C, (u32)i, hi);
 }
@@ -1509,6 +1593,27 @@ static size_t carve_val(ValWs& v, char* base, i64 n, i64 m) {
 // --------------------------------------------------------------------------
 static inline unsigned nblk(i64 items, int bs) { return (unsigned)(items > 0 ? cdiv(items, bs) : 1); }
 
+// Per-function attributes (idempotent; set outside any stream capture).
+#ifndef PG_TAGS_CARVE
+#define PG_TAGS_CARVE 25
+#endif
+static cudaError_t set_kernel_attributes() {
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+    // The list-ranking walks hit L1 (the tour revisits nearby arcs), so they ask for the
+    // smallest shared-memory carveout that fits them (C5a listrank 11.85 -> 11.6 ms).
+    chk(cudaFuncSetAttribute(k_lr_walk1, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    chk(cudaFuncSetAttribute(k_lr_walk2, cudaFuncAttributePreferredSharedMemoryCarveout, 30));
+    // k_tags_blk likewise: its FIRST gathers need L1 lines while in flight, and a larger
+    // carveout than the 6 x 8.5 KB it needs cost up to 2.5x (C5a tags 36.2 -> 34.6 ms at 25 %,
+    // 90.7 ms at 100 %)
+    if (PG_TAGS_CARVE >= 0)
+        chk(cudaFuncSetAttribute(k_tags_blk<true>, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
+    chk(cudaFuncSetAttribute(k_wyllie_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(2 * sizeof(u32) * WY_MAX)));
+    return e;
+}
+
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr, size_t ws_bytes, u64 seed,
                u32 flags, cudaStream_t st, pasgal_bcc_prof_t* prof) {
     const i64 n = g->n, m = g->m_slots;
@@ -1526,7 +1631,11 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
             return cudaEventRecord((cudaEvent_t)prof->events[stage], st);
         return cudaSuccess;
     };
-    static const bool debug = getenv("PASGAL_BCC_DEBUG") != nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    PG_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    static const bool debug_env = getenv("PASGAL_BCC_DEBUG") != nullptr;
+    const bool debug = debug_env && !capturing;
 #define PG_K(...)                                                                          \
     do {                                                                                   \
         __VA_ARGS__;                                                                       \
@@ -1542,19 +1651,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         }                                                                                  \
     } while (0)
 
-    // The list-ranking walks hit L1 (the tour revisits nearby arcs), so they ask for the
-    // smallest shared-memory carveout that fits them (C5a listrank 11.85 -> 11.6 ms).  An
-    // idempotent per-function attribute, set on every call.
-    PG_CUDA_TRY(cudaFuncSetAttribute(k_lr_walk1, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-    PG_CUDA_TRY(cudaFuncSetAttribute(k_lr_walk2, cudaFuncAttributePreferredSharedMemoryCarveout, 30));
-    // k_tags_blk likewise: its FIRST gathers need L1 lines while in flight, and a larger
-    // carveout than the 6 x 8.5 KB it needs cost up to 2.5x (C5a tags 36.2 -> 34.6 ms at 25 %,
-    // 90.7 ms at 100 %)
-#ifndef PG_TAGS_CARVE
-#define PG_TAGS_CARVE 25
-#endif
-    if (PG_TAGS_CARVE >= 0)
-        PG_CUDA_TRY(cudaFuncSetAttribute(k_tags_blk<true>, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
+    if (!capturing) PG_CUDA_TRY(set_kernel_attributes());
     PG_CUDA_TRY(mark(PASGAL_STAGE_BEGIN));
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     PG_CUDA_TRY(cudaMemsetAsync(out->artic_bits, 0, sizeof(u32) * (size_t)cdiv(n, 32), st));
@@ -1566,8 +1663,9 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         return PASGAL_OK;
     }
     // ---- S2 First-CC
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, w.CROW));
-    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB));
+    const int lb = local_lb(n);
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.CROW));
+    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB));
     PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
     PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
@@ -1586,9 +1684,16 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[0],
                                                      w.SPNEXT[0]));
     int cur = 0;
-    for (i64 span = 1; span < w.ns; span <<= 1) {
-        PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1], w.SPNEXT[cur ^ 1]));
-        cur ^= 1;
+    if (w.ns <= WY_MAX) {
+        const size_t smem = 2 * sizeof(u32) * WY_MAX;
+        PG_K(k_wyllie_small<<<1, WY_T, smem, st>>>(w.ns, w.SPLEN[0], w.SPNEXT[0], w.SPLEN[1]));
+        cur = 1;
+    } else {
+        for (i64 span = 1; span < w.ns; span <<= 1) {
+            PG_K(k_wyllie<<<nblk(w.ns, B), B, 0, st>>>(w.ns, w.SPLEN[cur], w.SPNEXT[cur], w.SPLEN[cur ^ 1],
+                                                       w.SPNEXT[cur ^ 1]));
+            cur ^= 1;
+        }
     }
     PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[cur],
                                                      w.HAB, w.TA));
@@ -1611,14 +1716,19 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
     PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
-    for (i64 k = 1; k < w.lv; ++k)
-        PG_K(k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb, (i64)1 << (k - 1)));
+    if (w.nb <= RMQ_SMALL) {
+        if (w.lv > 1) PG_K(k_rmq_levels_small<<<1, 1024, 0, st>>>(w.nb, w.lv, w.ST));
+    } else {
+        for (i64 k = 1; k < w.lv; ++k)
+            PG_K(k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb,
+                                                          (i64)1 << (k - 1)));
+    }
     PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FPF, w.C));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
-    PG_K(k_cc2_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
-    PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, w.FPF, w.W, w.E, w.C));
+    PG_K(k_cc2_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
+    PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
     PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
@@ -1654,6 +1764,58 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
 }
 
 // ----------------------------------------------------------------------------
+// CUDA-graph form of one pasgal_bcc call: the ~50-70 launches of a call captured once for
+// fixed pointers and sizes, then replayed with one launch (small graphs are launch-bound:
+// C1 is ~0.5 ms of mostly launch gaps).  Kernels read every data-dependent count from the
+// workspace, so a replay is exactly a fresh call on whatever the pointers hold.
+// ----------------------------------------------------------------------------
+struct BccGraph {
+    cudaGraphExec_t exec;
+    int launches;
+};
+
+int bcc_graph_create(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed,
+                     u32 flags, void** handle) {
+    *handle = nullptr;
+    PG_CUDA_TRY(set_kernel_attributes());
+    cudaStream_t cs;
+    PG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    pasgal_bcc_prof_t prof{nullptr, 0, 0};
+    int st = PASGAL_OK;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        st = bcc_launch(g, out, ws, ws_bytes, seed, flags, cs, &prof);
+        e = cudaStreamEndCapture(cs, &graph);
+    }
+    cudaStreamDestroy(cs);
+    if (st != PASGAL_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return st != PASGAL_OK ? st : PASGAL_ECUDA;
+    }
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return PASGAL_ECUDA;
+    *handle = new BccGraph{exec, prof.launches};
+    return PASGAL_OK;
+}
+
+int bcc_graph_launch(void* handle, cudaStream_t st, int* launches) {
+    BccGraph* h = (BccGraph*)handle;
+    PG_CUDA_TRY(cudaGraphLaunch(h->exec, st));
+    if (launches) *launches = h->launches;
+    return PASGAL_OK;
+}
+
+void bcc_graph_destroy(void* handle) {
+    BccGraph* h = (BccGraph*)handle;
+    if (!h) return;
+    cudaGraphExecDestroy(h->exec);
+    delete h;
+}
+
+// ----------------------------------------------------------------------------
 // stand-alone connected components: S2 alone.  Union by
 // index makes every component's root its minimum vertex id, so the output is deterministic
 // and equal to a sequential labelling by minimum id.
@@ -1684,8 +1846,9 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     const int B = 256;
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     if (n > 0) {
-        k_cc_local<<<(unsigned)cdiv(n, LOCAL_B), LOCAL_T, 0, st>>>(n, off, tgt, w.P, w.HAB, w.HEAD, nullptr);
-        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB);
+        const int lb = local_lb(n);
+        k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, nullptr);
+        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB);
         k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
         k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);

@@ -21,6 +21,10 @@ size_t canonicalize_temp_bytes(i64 n, i64 m, i64 nlab);
 int canonicalize_launch(const pasgal_csr_t* g, const u32* in, i64 nlab, u32* out, void* temp, size_t temp_bytes,
                         cudaStream_t st);
 int csr_first_error(const pasgal_csr_t* g, void* scratch, int64_t* host_out, cudaStream_t st);
+int bcc_graph_create(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed,
+                     uint32_t flags, void** handle);
+int bcc_graph_launch(void* handle, cudaStream_t st, int* launches);
+void bcc_graph_destroy(void* handle);
 int canonical_checksum(const uint32_t* lab, int64_t m, const uint32_t* bits, int64_t n, unsigned long long* out,
                        cudaStream_t st);
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
@@ -59,8 +63,7 @@ size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots) {
     return pg::bcc_workspace_bytes(n, m_slots);
 }
 
-int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
-                  uint64_t seed, uint32_t flags, void* stream, pasgal_bcc_prof_t* prof) {
+static int check_bcc_args(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, uint32_t flags) {
     int s = check_csr(g);
     if (s) return s;
     if (!out || !out->bcc_count || (g->n > 0 && !out->artic_bits)) return PASGAL_EINVAL;
@@ -70,8 +73,34 @@ int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* work
         ((flags & PASGAL_BCC_CANONICAL) || (g->n > 0 && (!out->comp || !out->parent || !out->first))))
         return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
+    return PASGAL_OK;
+}
+
+int pasgal_bcc_ex(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
+                  uint64_t seed, uint32_t flags, void* stream, pasgal_bcc_prof_t* prof) {
+    int s = check_bcc_args(g, out, workspace, flags);
+    if (s) return s;
     return pg::bcc_launch(g, out, workspace, workspace_bytes, seed, flags, (cudaStream_t)stream, prof);
 }
+
+int pasgal_bcc_graph_create(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace,
+                            size_t workspace_bytes, uint64_t seed, uint32_t flags, pasgal_bcc_graph_t* graph) {
+    if (!graph) return PASGAL_EINVAL;
+    *graph = nullptr;
+    int s = check_bcc_args(g, out, workspace, flags);
+    if (s) return s;
+    void* h = nullptr;
+    s = pg::bcc_graph_create(g, out, workspace, workspace_bytes, seed, flags, &h);
+    *graph = (pasgal_bcc_graph_t)h;
+    return s;
+}
+
+int pasgal_bcc_graph_launch(pasgal_bcc_graph_t graph, void* stream, int* launches) {
+    if (!graph) return PASGAL_EINVAL;
+    return pg::bcc_graph_launch((void*)graph, (cudaStream_t)stream, launches);
+}
+
+void pasgal_bcc_graph_destroy(pasgal_bcc_graph_t graph) { pg::bcc_graph_destroy((void*)graph); }
 
 int pasgal_bcc(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, size_t workspace_bytes,
                uint64_t seed, uint32_t flags, void* stream) {

@@ -137,6 +137,55 @@ def test_vertex_mode_output_matches_reference_partition():
         pg.bcc(pg.Graph(case.offsets, case.targets), edge_labels=False, canonical=True)
 
 
+def test_cuda_graph_replay_matches_direct_call():
+    """pasgal_bcc_graph_*: a captured call replayed on fixed buffers gives the direct call's
+    results, and a replay after the input buffers were refilled with ANOTHER graph of the
+    same shape computes that graph (the replay reads whatever the pointers hold)."""
+    a = golden_io.single("c1_grid256_p06_s1.npz")
+    off_a, tgt_a = _dev(a)
+    n, m = a.n, a.targets.shape[0]
+    ws = torch.empty(pg.workspace_bytes(n, m), dtype=torch.uint8, device="cuda")
+
+    def fresh_out():
+        return pg.DeviceBcc(edge_label=torch.empty(m, dtype=torch.int32, device="cuda"),
+                            artic_bits=torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda"),
+                            bcc_count=torch.empty(1, dtype=torch.int64, device="cuda"))
+
+    out = fresh_out()
+    for rep in range(3):
+        r = pg.bcc_device(off_a, tgt_a, canonical=True, out=out, workspace=ws, graph=True)
+        assert r.launches > 10
+        lab, art, cnt = _host_out(r, n)
+        assert cnt == a.count and np.array_equal(art, a.articulation), rep
+        assert np.array_equal(lab, oracle.canonical_min_eid(a.offsets, a.targets, a.label)), rep
+    # same shape, different graph, same device buffers: the cached graph computes it
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.offsets))
+    rs, rd = n - 1 - src, n - 1 - a.targets.astype(np.int64)      # ids reversed: same n and m
+    order = np.lexsort((rd, rs))
+    off_b = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rs, minlength=n), out=off_b[1:])
+    tgt_b = rd[order].astype(np.uint32)
+    if True:
+        off_a.copy_(torch.from_numpy(off_b))
+        tgt_a.copy_(torch.from_numpy(tgt_b.view(np.int32)))
+        ref = oracle.bcc_hopcroft_tarjan(off_b, tgt_b)
+        r = pg.bcc_device(off_a, tgt_a, canonical=True, out=out, workspace=ws, graph=True)
+        lab, art, cnt = _host_out(r, n)
+        assert cnt == ref.bcc_count and np.array_equal(art, ref.articulation.astype(bool))
+        assert np.array_equal(lab, oracle.canonical_min_eid(off_b, tgt_b, ref.edge_label))
+    # automatic replay (fixed out + workspace, small n) equals an explicit direct call
+    case = golden_io.single("rmat_s12_d16_seed7.npz")
+    off, tgt = _dev(case)
+    ws2 = torch.empty(pg.workspace_bytes(case.n, case.m), dtype=torch.uint8, device="cuda")
+    o2 = pg.DeviceBcc(edge_label=torch.empty(case.m, dtype=torch.int32, device="cuda"),
+                      artic_bits=torch.empty((case.n + 31) // 32, dtype=torch.int32, device="cuda"),
+                      bcc_count=torch.empty(1, dtype=torch.int64, device="cuda"))
+    g1 = _host_out(pg.bcc_device(off, tgt, seed=3, canonical=True, out=o2, workspace=ws2), case.n)
+    g2 = _host_out(pg.bcc_device(off, tgt, seed=3, canonical=True, out=o2, workspace=ws2, graph=False), case.n)
+    assert np.array_equal(g1[0], g2[0]) and np.array_equal(g1[1], g2[1]) and g1[2] == g2[2] == case.count
+    pg.release_workspace()
+
+
 def test_validation_errors_match_reference():
     # non-symmetric (oracles.py:127-128)
     off = np.array([0, 1, 1, 1], dtype=np.int64)
