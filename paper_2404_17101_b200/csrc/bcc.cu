@@ -72,7 +72,13 @@ struct Ctr {
     u32 nvheavy;  // very heavy rows queued by k_cc_rest (HEAVY back, from index n-1 down)
     u32 nvheavy2; // very heavy rows queued by k_cc2_rest (HEAVY back)
     u32 gcid;     // component id (head preorder rank) of the sampled giant skeleton component
+    u32 nfr;      // VGC First-CC: claimed vertices whose rows await the frontier pass (FR)
+    u32 cc_vgc;   // First-CC path chosen by k_cc_policy: 1 = VGC local searches, 0 = sampled union-find
 };
+
+// Kernels of the two First-CC paths are all launched (a static launch sequence, capturable
+// in a CUDA graph); the ones of the path k_cc_policy did not choose return at once.
+__device__ __forceinline__ bool gated_off(const u32* gate, u32 want) { return gate && ldcg(gate) != want; }
 
 // --------------------------------------------------------------------------
 // workspace carve-up (identical for sizing and use)
@@ -234,8 +240,9 @@ __device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
 // entries of all the chunks that start inside it).
 __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, int lb, const i64* __restrict__ off,
                                                       const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
-                                                      u32* HEAD, u32* CROW) {
+                                                      u32* HEAD, u32* CROW, const u32* gate) {
     __shared__ u32 sp[LOCAL_B];
+    if (gated_off(gate, 0)) return;
     const i64 b0 = (i64)blockIdx.x << lb;
     const int cnt = (int)(n - b0 < (1 << lb) ? n - b0 : (1 << lb));
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
@@ -287,9 +294,9 @@ __device__ __forceinline__ void uf_find_lockstep(u32* P, u32 (&x)[K]) {
 }
 
 __global__ void k_cc_sample(i64 n, int lb, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
-                            uint2* HAB) {
+                            uint2* HAB, const u32* gate) {
     i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
+    if (v >= n || gated_off(gate, 0)) return;
     i64 a = off[v], b = off[v + 1];
     u32 t[NSAMPLE], x[NSAMPLE + 1];
     bool act[NSAMPLE], any = false;
@@ -376,7 +383,8 @@ __device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i6
 #define PG_CMP_MINB 2
 #endif
 template <int ILP>
-__global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i64 n, u32* P) {
+__global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i64 n, u32* P, const u32* gate) {
+    if (gated_off(gate, 0)) return;
     u32 root[ILP];
     i64 idx[ILP];
     compress_ilp<ILP>(n, P, root, idx);
@@ -386,7 +394,8 @@ __global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i
 // a shared-memory open-addressing table (one insert per thread) instead of every thread
 // scanning all samples (O(S^2) shared loads: 24 us per call, a visible share at C1).
 constexpr int GIANT_HASH = 2 * GIANT_SAMPLES;
-__global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u64 seed, u32* out) {
+__global__ void __launch_bounds__(GIANT_SAMPLES) k_giant(i64 n, const u32* P, u64 seed, u32* out, const u32* gate) {
+    if (gated_off(gate, 0)) return;
     __shared__ u32 hk[GIANT_HASH], hc[GIANT_HASH];
     typedef cub::BlockReduce<u64, GIANT_SAMPLES> BR;
     __shared__ typename BR::TempStorage tmp;
@@ -426,9 +435,9 @@ __device__ __forceinline__ void queue_heavy(i64 n, i64 len, u32 u, u32* heavy, u
 }
 
 __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
-                          Ctr* ctr, u32* heavy) {
+                          Ctr* ctr, u32* heavy, const u32* gate) {
     i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
+    if (u >= n || gated_off(gate, 0)) return;
     i64 a = off[u] + NSAMPLE, b = off[u + 1];
     if (a >= b || ldcg(P + u) == ctr->giant) return;
     if (b - a > HEAVY_ROW) {
@@ -438,12 +447,14 @@ __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __r
     for (i64 s = a; s < b; ++s) uf_link_hook(P, (u32)u, (u32)tgt[s], HAB);
 }
 
+template <int SKIP>
 __global__ void k_cc_rest_heavy(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
-                                uint2* HAB, const Ctr* ctr, const u32* __restrict__ heavy) {
+                                uint2* HAB, const Ctr* ctr, const u32* __restrict__ heavy, const u32* gate, u32 want) {
+    if (gated_off(gate, want)) return;
     const u32 nh = ctr->nheavy, nvh = ctr->nvheavy;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         u32 u = heavy[h];
-        i64 a = off[u] + NSAMPLE, b = off[u + 1];
+        i64 a = off[u] + SKIP, b = off[u + 1];
         for (i64 s = a + threadIdx.x; s < b; s += blockDim.x) {
             const int32_t w = tgt[s];
             if (s > off[u] && tgt[s - 1] == w) continue;
@@ -452,11 +463,260 @@ __global__ void k_cc_rest_heavy(i64 n, const i64* __restrict__ off, const int32_
     }
     for (u32 h = 0; h < nvh; ++h) {
         u32 u = heavy[n - 1 - h];
-        i64 a = off[u] + NSAMPLE, b = off[u + 1];
+        i64 a = off[u] + SKIP, b = off[u + 1];
         for (i64 s = a + (i64)blockIdx.x * blockDim.x + threadIdx.x; s < b; s += (i64)gridDim.x * blockDim.x) {
             const int32_t w = tgt[s];
             if (s > off[u] && tgt[s - 1] == w) continue;
             uf_link_hook(P, u, (u32)w, HAB);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// S2, VGC form (north-star item 2; the paper's vertical granularity control, PAPER.md
+// "Vertical Granularity Control", SPEC.md vgc-engine local_search): for sparse graphs
+// (grids, kNN, roads: few slots per vertex, large diameter) the spanning forest is grown by
+// per-warp multi-hop local searches instead of sampled union-find.
+//
+//   k_vgc_search  persistent warps; warp k scans its id range for unclaimed vertices and
+//                 makes each a seed (CAS P[v]: INV -> v).  From a seed it runs a bounded
+//                 BFS-order local search: its queue lives in shared memory, 32 queued
+//                 vertices are expanded at once (one per lane), every neighbour still
+//                 unclaimed is claimed for the seed (CAS P[w]: INV -> seed) with the edge
+//                 that reached it as its forest edge (HAB[w]), and the search stops once
+//                 tau vertices are processed -- so one search advances many hops and a
+//                 large-diameter graph needs no per-level global rounds.  A neighbour
+//                 claimed by ANOTHER search joins the two search trees in the union-find
+//                 over seeds (uf_link_hook: the hook edge is the forest edge).  Queue
+//                 overflow, the queue left when the search stops, and rows longer than
+//                 VGC_HEAVY slots go to the frontier list FR (their rows are not yet read).
+//   k_vgc_rest    every vertex is claimed by now; the FR rows link their neighbours' trees
+//                 (thread per row; long rows to the block-per-row list of k_cc_rest_heavy).
+//
+// P[w] = seed for a claimed vertex and P[s] = s (or its hook) for a seed, so the roots are
+// exactly the never-hooked seeds (P[x] == x) and every other vertex owns one forest edge in
+// HAB, which is all the later stages use.  Claims build one tree per search; each hook
+// joins two union-find trees through one edge, so the edges form a spanning forest.
+// --------------------------------------------------------------------------
+constexpr int VGC_WARPS = 4;          // warps per block
+#ifndef PG_VGC_Q
+#define PG_VGC_Q 256
+#endif
+constexpr int VGC_Q = PG_VGC_Q;            // per-warp queue capacity (ring of (vertex, seed), shared memory)
+constexpr int VGC_HEAVY = 32;         // longer rows are deferred to the frontier pass
+constexpr int VGC_TAU_DEFAULT = 1024; // vertices processed per local search (SPEC tau)
+
+// First-CC policy, on the device (no host synchronisation): VGC local searches for a
+// sparse graph (at most VGC_MAX_DEG slots per vertex on average) whose ids are LOCAL -- the
+// first neighbour of most sampled vertices lies within n/256 ids (grids, meshes, road
+// networks in their usual orderings) -- so that the searches' row reads and claims stay in
+// cache; sampled union-find with the giant-component skip otherwise (dense or power-law
+// graphs, where it reads only a few slots of most rows, and random-id graphs such as C4's
+// kNN, where a search's every row read is a random line).  mode 1/2 forces VGC/union-find.
+constexpr i64 VGC_MAX_DEG = 8;
+constexpr i64 VGC_MIN_N = 1 << 18;   // below: launch/latency-bound, the id-block path is faster (C1)
+constexpr int POLICY_SAMPLES = 1024;
+__global__ void __launch_bounds__(POLICY_SAMPLES) k_cc_policy(i64 n, i64 m, const i64* __restrict__ off,
+                                                              const int32_t* __restrict__ tgt, u64 seed, int mode,
+                                                              Ctr* ctr) {
+    __shared__ u32 nloc, nsamp;
+    if (threadIdx.x == 0) nloc = nsamp = 0;
+    __syncthreads();
+    const u32 v = (u32)(draw(seed ^ 0x9011C7ull, threadIdx.x) % (u64)n);
+    const i64 a = off[v], b = off[(i64)v + 1];
+    if (b > a) {
+        const i64 w = tgt[a];
+        const i64 d = w > (i64)v ? w - (i64)v : (i64)v - w;
+        atomicAdd(&nsamp, 1u);
+        if (d <= (n >> 8) || d <= 64) atomicAdd(&nloc, 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        ctr->cc_vgc = mode == 1   ? 1u
+                      : mode == 2 ? 0u
+                                  : (n >= VGC_MIN_N && m <= VGC_MAX_DEG * n && 2 * nloc > nsamp) ? 1u : 0u;
+}
+
+__global__ void k_vgc_init(i64 n, const i64* __restrict__ off, u32* P, uint2* HAB, u32* HEAD, u32* CROW,
+                           const u32* gate) {
+    const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || gated_off(gate, 1)) return;
+    P[v] = PG_INV;
+    reinterpret_cast<uint4*>(HAB)[v] = make_uint4(PG_INV, PG_INV, 0u, 0u);
+    HEAD[v] = PG_INV;
+    if (CROW) {
+        const i64 a = off[v], b = off[v + 1];
+        for (i64 c = cdiv(a, WCH); c * WCH < b; ++c) CROW[c] = (u32)v;
+    }
+}
+
+__device__ __forceinline__ void vgc_push_frontier(u32* FR, Ctr* ctr, bool push, u32 x, int lane) {
+    const unsigned pm = __ballot_sync(0xFFFFFFFFu, push);
+    if (!pm) return;
+    const int lead = __ffs(pm) - 1;
+    u32 base = 0;
+    if (lane == lead) base = atomicAdd(&ctr->nfr, (u32)__popc(pm));
+    base = __shfl_sync(0xFFFFFFFFu, base, lead);
+    if (push) FR[base + __popc(pm & ((1u << lane) - 1u))] = x;
+}
+
+// The warp's search loop.  Queue entries are (vertex, seed of its tree).  Each step
+// expands up to 32 queued vertices at once: their rows are flattened over the lanes (a scan
+// of the row lengths; each lane finds its slot's row by a 5-step shuffle search), and
+// VGC_K slots per lane go through target load, claim check and claim CAS together, so a
+// step costs a few dependent memory round trips whatever the row lengths.  Whenever fewer
+// than 32 vertices are queued the warp starts new searches from the next unclaimed ids of
+// its range, so the many small clusters of a sparse graph (a p = 0.6 grid) are searched
+// several at a time instead of one short, latency-bound search after another.  After tau
+// expansions the queue is flushed to the frontier and the warp starts afresh.
+constexpr int VGC_K = 4;
+__global__ void __launch_bounds__(VGC_WARPS * 32, 8) k_vgc_search(i64 n, const i64* __restrict__ off,
+                                                               const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                                                               u32* FR, Ctr* ctr, int tau, const u32* gate) {
+    __shared__ uint2 qs[VGC_WARPS][VGC_Q];
+    if (gated_off(gate, 1)) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    uint2* Q = qs[wib];
+    const i64 nw = (i64)gridDim.x * VGC_WARPS;
+    const i64 wid = (i64)blockIdx.x * VGC_WARPS + wib;
+    const i64 r0 = n * wid / nw, r1 = n * (wid + 1) / nw;
+    i64 v0 = r0 - 32;          // current scan group [v0, v0 + 32)
+    unsigned cm = 0;           // its unclaimed candidates not yet tried
+    bool scanning = r0 < r1;
+    u32 head = 0, tail = 0;    // monotone counters; slot = counter % VGC_Q
+    int processed = 0;
+    for (;;) {
+        // refill with new seeds while the next step would run below a full warp
+        while (scanning && tail - head < 32u) {
+            if (!cm) {
+                v0 += 32;
+                if (v0 >= r1) {
+                    scanning = false;
+                    break;
+                }
+                const i64 v = v0 + lane;
+                cm = __ballot_sync(0xFFFFFFFFu, v < r1 && ldcg(P + v) == PG_INV);
+                continue;
+            }
+            const u32 need = 32u - (tail - head);
+            unsigned take = cm;                         // the first `need` candidates
+            while ((u32)__popc(take) > need) take &= ~(1u << (31 - __clz(take)));
+            cm &= ~take;
+            const u32 v = (u32)(v0 + lane);
+            bool ok = false;
+            if ((take >> lane) & 1u) ok = atomicCAS(P + v, PG_INV, v) == PG_INV;
+            const unsigned okm = __ballot_sync(0xFFFFFFFFu, ok);
+            if (ok) Q[(tail + (u32)__popc(okm & lt)) % VGC_Q] = make_uint2(v, v);
+            tail += (u32)__popc(okm);
+        }
+        if (head == tail) break;
+        const u32 cnt = tail - head < 32u ? tail - head : 32u;
+        const bool has = (u32)lane < cnt;
+        const uint2 ent = has ? Q[(head + lane) % VGC_Q] : make_uint2(0u, 0u);
+        const u32 u = ent.x, sd = ent.y;
+        head += cnt;
+        processed += (int)cnt;
+        i64 a = 0, b = 0;
+        if (has) {
+            a = off[u];
+            b = off[(i64)u + 1];
+        }
+        const bool heavy = has && b - a > VGC_HEAVY;
+        vgc_push_frontier(FR, ctr, heavy, u, lane);
+        const u32 deg = has && !heavy ? (u32)(b - a) : 0u;
+        u32 incl = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const u32 excl = incl - deg;
+        u32 last_o = PG_INV;
+        for (u32 base = 0; base < total; base += 32 * VGC_K) {
+            u32 w[VGC_K], su[VGC_K], ss[VGC_K], o[VGC_K];
+            bool act[VGC_K], claimed[VGC_K];
+#pragma unroll
+            for (int k = 0; k < VGC_K; ++k) {
+                const u32 t = base + 32 * k + lane;
+                act[k] = t < total;
+                int j = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const u32 ex = __shfl_sync(0xFFFFFFFFu, excl, j + step < 32 ? j + step : 31);
+                    if (j + step < 32 && ex <= t) j += step;
+                }
+                su[k] = __shfl_sync(0xFFFFFFFFu, u, j);
+                ss[k] = __shfl_sync(0xFFFFFFFFu, sd, j);
+                const i64 aj = __shfl_sync(0xFFFFFFFFu, a, j);
+                const u32 ej = __shfl_sync(0xFFFFFFFFu, excl, j);
+                w[k] = act[k] ? (u32)tgt[aj + (t - ej)] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < VGC_K; ++k) o[k] = act[k] ? ldcg(P + w[k]) : ss[k];
+#pragma unroll
+            for (int k = 0; k < VGC_K; ++k) {
+                claimed[k] = false;
+                if (o[k] == PG_INV) {
+                    o[k] = atomicCAS(P + w[k], PG_INV, ss[k]);
+                    if (o[k] == PG_INV) {
+                        claimed[k] = true;
+                        HAB[2 * (size_t)w[k]] = make_uint2(su[k], w[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < VGC_K; ++k) {
+                if (act[k] && !claimed[k] && o[k] != ss[k] && o[k] != last_o) {   // another tree: join
+                    uf_link_hook(P, su[k], w[k], HAB);
+                    last_o = o[k];
+                }
+                const unsigned cb = __ballot_sync(0xFFFFFFFFu, claimed[k]);
+                if (cb) {
+                    const u32 room = VGC_Q - (tail - head);
+                    const u32 r = (u32)__popc(cb & lt);
+                    const bool fits = claimed[k] && r < room;
+                    if (fits) Q[(tail + r) % VGC_Q] = make_uint2(w[k], ss[k]);
+                    vgc_push_frontier(FR, ctr, claimed[k] && !fits, w[k], lane);
+                    const u32 tot = (u32)__popc(cb);
+                    tail += tot < room ? tot : room;
+                }
+            }
+        }
+        __syncwarp();
+        if (processed >= tau) {     // flush: the unexpanded queue's rows go to the frontier pass
+            const u32 rem = tail - head;
+            if (rem) {
+                u32 fb = 0;
+                if (lane == 0) fb = atomicAdd(&ctr->nfr, rem);
+                fb = __shfl_sync(0xFFFFFFFFu, fb, 0);
+                for (u32 q = lane; q < rem; q += 32) FR[fb + q] = Q[(head + q) % VGC_Q].x;
+            }
+            head = tail;
+            processed = 0;
+            __syncwarp();
+        }
+    }
+}
+
+// frontier rows: link every neighbour's tree (all vertices are claimed); long rows go to
+// the block-per-row list (k_cc_rest_heavy with skip 0)
+__global__ void k_vgc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                           const u32* __restrict__ FR, Ctr* ctr, u32* heavy, const u32* gate) {
+    if (gated_off(gate, 1)) return;
+    const u32 nfr = ctr->nfr;
+    for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < nfr; k += gridDim.x * blockDim.x) {
+        const u32 u = FR[k];
+        const i64 a = off[u], b = off[(i64)u + 1];
+        if (b - a > HEAVY_ROW) {
+            queue_heavy(n, b - a, u, heavy, &ctr->nheavy, &ctr->nvheavy);
+            continue;
+        }
+        const u32 ou = ldcg(P + u);
+        for (i64 sl = a; sl < b; ++sl) {
+            const u32 w = (u32)tgt[sl];
+            if (ldcg(P + w) != ou) uf_link_hook(P, u, w, HAB);
         }
     }
 }
@@ -1593,6 +1853,31 @@ static size_t carve_val(ValWs& v, char* base, i64 n, i64 m) {
 // --------------------------------------------------------------------------
 static inline unsigned nblk(i64 items, int bs) { return (unsigned)(items > 0 ? cdiv(items, bs) : 1); }
 
+// First-CC knobs for sweeps: PASGAL_BCC_CC=vgc|afforest forces a path (k_cc_policy
+// decides otherwise), PASGAL_BCC_VGC_TAU sets tau.
+static int cc_mode() {
+    const char* e = getenv("PASGAL_BCC_CC");
+    return e && e[0] == 'v' ? 1 : e && e[0] == 'a' ? 2 : 0;
+}
+static int vgc_tau() {
+    const char* t = getenv("PASGAL_BCC_VGC_TAU");
+    return t && atoi(t) > 0 ? atoi(t) : VGC_TAU_DEFAULT;
+}
+static unsigned vgc_grid() {
+    static int blocks = 0;
+    if (!blocks) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgc_search, VGC_WARPS * 32, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        blocks = per_sm * sms;
+    }
+    return (unsigned)blocks;
+}
+
 // Per-function attributes (idempotent; set outside any stream capture).
 #ifndef PG_TAGS_CARVE
 #define PG_TAGS_CARVE 25
@@ -1611,6 +1896,7 @@ static cudaError_t set_kernel_attributes() {
         chk(cudaFuncSetAttribute(k_tags_blk<true>, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
     chk(cudaFuncSetAttribute(k_wyllie_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(2 * sizeof(u32) * WY_MAX)));
+    (void)vgc_grid();   // occupancy query cached outside any capture
     return e;
 }
 
@@ -1662,14 +1948,23 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         if (prof) prof->launches = nl;
         return PASGAL_OK;
     }
-    // ---- S2 First-CC
+    // ---- S2 First-CC: VGC local searches on sparse local-id graphs, sampled union-find
+    // otherwise (k_cc_policy decides on the device; the other path's kernels return at once)
     const int lb = local_lb(n);
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.CROW));
-    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB));
-    PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P));
-    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant));
-    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
-    PG_K(k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY));
+    const u32* gate = &w.ctr->cc_vgc;
+    PG_K(k_cc_policy<<<1, POLICY_SAMPLES, 0, st>>>(n, m, off, tgt, seed, cc_mode(), w.ctr));
+    PG_K(k_vgc_init<<<nblk(n, B), B, 0, st>>>(n, off, w.P, w.HAB, w.HEAD, w.CROW, gate));
+    PG_K(k_vgc_search<<<vgc_grid(), VGC_WARPS * 32, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, vgc_tau(),
+                                                             gate));
+    PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, w.HEAVY, gate));
+    PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 1));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.CROW,
+                                                                         gate));
+    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, gate));
+    PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, gate));
+    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant, gate));
+    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate));
+    PG_K(k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 0));
     // no final compress: later stages only ask "is x a root", and P[x] == x exactly at roots
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
@@ -1729,8 +2024,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // ---- S5 Last-CC over cross edges
     PG_K(k_cc2_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
     PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
-    PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C));
-    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2));
+    PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C, nullptr));
+    PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2, nullptr));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
     PG_K(k_compress_final<<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C, w.ctr));
@@ -1847,13 +2142,14 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     if (n > 0) {
         const int lb = local_lb(n);
-        k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, nullptr);
-        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB);
-        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
-        k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant);
-        k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
-        k_cc_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY);
-        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P);
+        k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, nullptr,
+                                                                        nullptr);
+        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, nullptr);
+        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, nullptr);
+        k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant, nullptr);
+        k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, nullptr);
+        k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, nullptr, 0);
+        k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, nullptr);
         k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
     }
     k_cc_count<<<1, 1, 0, st>>>(w.ctr, count_dev);
