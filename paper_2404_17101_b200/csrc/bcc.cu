@@ -80,6 +80,7 @@ struct Ctr {
 // in a CUDA graph); the ones of the path k_cc_policy did not choose return at once.
 __device__ __forceinline__ bool gated_off(const u32* gate, u32 want) { return gate && ldcg(gate) != want; }
 
+
 // --------------------------------------------------------------------------
 // workspace carve-up (identical for sizing and use)
 // --------------------------------------------------------------------------
@@ -293,10 +294,17 @@ __device__ __forceinline__ void uf_find_lockstep(u32* P, u32 (&x)[K]) {
     }
 }
 
+__device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restrict__ off,
+                                              const int32_t* __restrict__ tgt, u32* P, uint2* HAB);
 __global__ void k_cc_sample(i64 n, int lb, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
                             uint2* HAB, const u32* gate) {
-    i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n || gated_off(gate, 0)) return;
+    cc_sample_one(v, lb, off, tgt, P, HAB);
+}
+
+__device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restrict__ off,
+                                              const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
     i64 a = off[v], b = off[v + 1];
     u32 t[NSAMPLE], x[NSAMPLE + 1];
     bool act[NSAMPLE], any = false;
@@ -436,7 +444,7 @@ __device__ __forceinline__ void queue_heavy(i64 n, i64 len, u32 u, u32* heavy, u
 
 __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
                           Ctr* ctr, u32* heavy, const u32* gate) {
-    i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n || gated_off(gate, 0)) return;
     i64 a = off[u] + NSAMPLE, b = off[u + 1];
     if (a >= b || ldcg(P + u) == ctr->giant) return;
@@ -539,14 +547,15 @@ __global__ void __launch_bounds__(POLICY_SAMPLES) k_cc_policy(i64 n, i64 m, cons
 
 __global__ void k_vgc_init(i64 n, const i64* __restrict__ off, u32* P, uint2* HAB, u32* HEAD, u32* CROW,
                            const u32* gate) {
-    const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n || gated_off(gate, 1)) return;
-    P[v] = PG_INV;
-    reinterpret_cast<uint4*>(HAB)[v] = make_uint4(PG_INV, PG_INV, 0u, 0u);
-    HEAD[v] = PG_INV;
-    if (CROW) {
-        const i64 a = off[v], b = off[v + 1];
-        for (i64 c = cdiv(a, WCH); c * WCH < b; ++c) CROW[c] = (u32)v;
+    if (gated_off(gate, 1)) return;
+    for (i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (i64)gridDim.x * blockDim.x) {
+        P[v] = PG_INV;
+        reinterpret_cast<uint4*>(HAB)[v] = make_uint4(PG_INV, PG_INV, 0u, 0u);
+        HEAD[v] = PG_INV;
+        if (CROW) {
+            const i64 a = off[v], b = off[v + 1];
+            for (i64 c = cdiv(a, WCH); c * WCH < b; ++c) CROW[c] = (u32)v;
+        }
     }
 }
 
@@ -757,6 +766,51 @@ __device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc
     old = __shfl_sync(g.grp, old, g.lead);
     u32 nxt = __shfl_sync(g.grp, arc, g.later ? __ffs(g.later) - 1 : (threadIdx.x & 31));
     NEXT[arc] = g.later ? nxt : old;   // the group's last arc continues into the old list
+}
+
+// Block-aggregated form (default): a block's AL_T hooked vertices insert their 2 AL_T arcs
+// into a shared-memory table keyed by source vertex, chaining arcs of one source locally
+// (shared-memory exchanges), then splice each local chain into the global list with ONE
+// atomicExch per distinct source per block.  On a power-law forest most arcs leave a few
+// hubs: per-warp aggregation still left ~5M returning exchanges on the top hub's HEAD,
+// serialised at one L2 slice; per-block aggregation divides that by the block size and
+// keeps each hub's list in runs of consecutive hooked ids.
+constexpr int AL_T = 1024, AL_H = 4096;
+__global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
+    __shared__ u32 hkey[AL_H], hhead[AL_H], htail[AL_H];
+    for (int i = threadIdx.x; i < AL_H; i += AL_T) {
+        hkey[i] = PG_INV;
+        hhead[i] = PG_INV;
+    }
+    __syncthreads();
+    const i64 x = (i64)blockIdx.x * AL_T + threadIdx.x;
+    const uint2 e = x < n ? HAB[2 * x] : make_uint2(PG_INV, PG_INV);
+    if (e.x != PG_INV) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const u32 key = d ? e.y : e.x, arc = 2 * (u32)x + d;
+            u32 h = (key * 0x9E3779B1u) >> (32 - 12);     // AL_H = 2^12 slots
+            for (;;) {
+                const u32 k = atomicCAS(hkey + h, PG_INV, key);
+                if (k == PG_INV || k == key) break;
+                h = (h + 1) & (AL_H - 1);
+            }
+            const u32 old = atomicExch(hhead + h, arc);
+            if (old == PG_INV) htail[h] = arc;             // first in: the local chain's tail
+            else NEXT[arc] = old;
+        }
+    }
+    __syncthreads();
+    u32 key[AL_H / AL_T], old[AL_H / AL_T];
+#pragma unroll
+    for (int j = 0; j < AL_H / AL_T; ++j) {                 // the exchanges in flight together
+        const int h = threadIdx.x + j * AL_T;
+        key[j] = hkey[h];
+        old[j] = key[j] != PG_INV ? atomicExch(HEAD + key[j], hhead[h]) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < AL_H / AL_T; ++j)
+        if (key[j] != PG_INV) NEXT[htail[threadIdx.x + j * AL_T]] = old[j];
 }
 
 __global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
@@ -1951,13 +2005,23 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // ---- S2 First-CC: VGC local searches on sparse local-id graphs, sampled union-find
     // otherwise (k_cc_policy decides on the device; the other path's kernels return at once)
     const int lb = local_lb(n);
-    const u32* gate = &w.ctr->cc_vgc;
-    PG_K(k_cc_policy<<<1, POLICY_SAMPLES, 0, st>>>(n, m, off, tgt, seed, cc_mode(), w.ctr));
-    PG_K(k_vgc_init<<<nblk(n, B), B, 0, st>>>(n, off, w.P, w.HAB, w.HEAD, w.CROW, gate));
-    PG_K(k_vgc_search<<<vgc_grid(), VGC_WARPS * 32, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, vgc_tau(),
-                                                             gate));
-    PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, w.HEAVY, gate));
-    PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 1));
+    // VGC is a candidate only for sparse graphs (host-known sizes); then k_cc_policy picks
+    // on the device and the other path's kernels return at once.  k_vgc_init runs
+    // grid-stride on a capped grid; k_cc_sample / k_cc_rest keep one vertex per thread of a
+    // full grid (a capped grid-stride or chunked form let the in-flight vertices spread over
+    // the id range: C4 k_cc_sample 3.0 -> 8.3 ms), which costs ~0.1 ms when skipped (C3)
+    const int mode = cc_mode();
+    const bool vgc_possible = mode == 1 || (mode == 0 && n >= VGC_MIN_N && m <= VGC_MAX_DEG * n);
+    const u32* gate = vgc_possible ? &w.ctr->cc_vgc : nullptr;
+    const unsigned capped = (unsigned)(nblk(n, B) < 148 * 8 ? nblk(n, B) : 148 * 8);
+    if (vgc_possible) {
+        PG_K(k_cc_policy<<<1, POLICY_SAMPLES, 0, st>>>(n, m, off, tgt, seed, mode, w.ctr));
+        PG_K(k_vgc_init<<<capped, B, 0, st>>>(n, off, w.P, w.HAB, w.HEAD, w.CROW, gate));
+        PG_K(k_vgc_search<<<vgc_grid(), VGC_WARPS * 32, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, vgc_tau(),
+                                                                 gate));
+        PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, w.HEAVY, gate));
+        PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 1));
+    }
     PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.CROW,
                                                                          gate));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, gate));
@@ -1969,7 +2033,10 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
-    PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    if (getenv("PASGAL_BCC_ARC_WARP"))
+        PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    else
+        PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
     PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
         n, w.HAB, w.HEAD, w.P, w.ctr, w.NEXT,
         IsoOut{w.FL, w.PV, w.E, w.PPAR, w.W, w.ROOTMARK}));
