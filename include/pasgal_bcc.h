@@ -273,6 +273,19 @@ int pasgal_msbfs_ex(const pasgal_csr_t* g, const int64_t* sources, int nsources,
                     int64_t* levels, const int32_t* probe, int64_t nprobe, int32_t* probe_dist, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* VGC frontier engine (SPEC.md vgc-engine run_frontier_loop / local_search, bfs
+ * bfs_parallel; PAPER.md "Vertical Granularity Control"), instantiated for
+ * exact BFS hop distances from `source` on any CSR (directed or symmetric).  Each round
+ * expands the packed frontier by per-warp local searches that process at least `tau`
+ * vertices (tau >= 1), possibly many hops deep, with write-min distances; improvements
+ * beyond a search's budget form the next frontier.  dist (device int32[n]) = hop distance,
+ * -1 if unreachable (oracles.bfs_queue, oracles.py:27-46, exactly); *rounds (host) = rounds
+ * executed (tau = 1: the eccentricity of the source + 1).  SYNCHRONISES `stream`.
+ * Workspace: pasgal_bfs_vgc_workspace_bytes(n). */
+size_t pasgal_bfs_vgc_workspace_bytes(int64_t n);
+int pasgal_bfs_vgc(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
 /* Articulation bitmap -> one byte per vertex (0/1), on the device: the reference's
  * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.
  * Asynchronous on `stream`. */

@@ -14,11 +14,12 @@ from .bcc import articulation_bytes_device, bcc, bcc_device, release_workspace, 
 
 from .io import GraphFormatError, load_adj, load_bin, load_graph, save_adj, save_bin
 from .pipeline import BccPipeline
-from .bfs import UNREACHED, DistanceArray, GraphStats, bfs, eccentricities, estimate_diameter
+from .bfs import UNREACHED, DistanceArray, GraphStats, VgcConfig, bfs, bfs_parallel, eccentricities, estimate_diameter
 
 __all__ = [
     "GraphFormatError", "load_adj", "load_bin", "load_graph", "save_adj", "save_bin",
-    "BccPipeline", "UNREACHED", "DistanceArray", "GraphStats", "bfs", "eccentricities", "estimate_diameter",
+    "BccPipeline", "UNREACHED", "DistanceArray", "GraphStats", "VgcConfig", "bfs", "bfs_parallel", "eccentricities",
+    "estimate_diameter",
     "BccLabels", "canonical_checksum", "canonical_edge_partition", "canonical_relabel", "min_eid_to_partition",
     "CONFIGS", "DeviceGraph", "Graph", "csr_from_keys", "gen_grid", "gen_knn", "gen_rmat", "make_config",
     "symmetrize_edges", "DeviceBcc", "HostBuffers", "connected_components", "connected_components_device", "canonical_checksum_device", "canonicalize_device", "same_partition_device", "articulation_bytes_device", "bcc", "bcc_device", "release_workspace", "unpack_articulation",

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpasgal_bcc.so")
-SOURCES = ["bcc.cu", "gen.cu", "sort.cu", "adj.cu", "bfs.cu", "capi.cu"]
+SOURCES = ["bcc.cu", "gen.cu", "sort.cu", "adj.cu", "bfs.cu", "vgc.cu", "capi.cu"]
 HEADERS = ["common.cuh", "scan.cuh", "wchunk.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -78,6 +78,9 @@ SIGNATURES = {
     "pasgal_gen_knn_keys": (_INT, [_I64, _INT, _U64, _INT, _VP, _VP, _VP, _SZ, _VP]),
     "pasgal_bits_to_bytes": (_INT, [_VP, _I64, _VP, _VP]),
     "pasgal_canonical_checksum": (_INT, [_VP, _I64, _VP, _I64, _VP, _VP]),
+    "pasgal_bfs_vgc_workspace_bytes": (_SZ, [_I64]),
+    "pasgal_bfs_vgc": (_INT, [ctypes.POINTER(PasgalCsr), _I64, _INT, _VP, ctypes.POINTER(ctypes.c_int64), _VP, _SZ,
+                              _VP]),
     "pasgal_adj_temp_bytes": (_SZ, [_I64]),
     "pasgal_msbfs_workspace_bytes": (_SZ, [_I64]),
     "pasgal_msbfs": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(ctypes.c_int64), _INT, _VP,

@@ -8,7 +8,7 @@ mkdir -p $OUT
 while [ $# -ge 2 ]; do
   name=$1; defs=$2; shift 2
   d=$(mktemp -d)
-  for f in bcc gen sort adj bfs capi; do
+  for f in bcc gen sort adj bfs vgc capi; do
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $defs \
       -c paper_2404_17101_b200/csrc/$f.cu -o $d/$f.o &
   done
