@@ -134,7 +134,7 @@ def validate_device(offsets, targets, workspace=None):
     _lib.check(st, "validate")
 
 
-GRAPH_MAX_N = 1 << 22       # auto CUDA-graph replay below this size (launch-bound calls)
+GRAPH_MAX_N = 1 << 26       # auto CUDA-graph replay below this size (launch gaps matter up to C4)
 _GRAPH_CACHE_SIZE = 8
 
 
