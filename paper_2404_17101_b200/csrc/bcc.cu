@@ -241,7 +241,7 @@ __device__ __forceinline__ u32 slink(u32* sp, u32 a, u32 b) {
 // entries of all the chunks that start inside it).
 __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, int lb, const i64* __restrict__ off,
                                                       const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
-                                                      u32* HEAD, u32* CROW, const u32* gate) {
+                                                      u32* HEAD, u32* NEXT, u32* CROW, const u32* gate) {
     __shared__ u32 sp[LOCAL_B];
     if (gated_off(gate, 0)) return;
     const i64 b0 = (i64)blockIdx.x << lb;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc_local(i64 n, int lb, const i64* 
             i64 w = tgt[a + k];
             if ((w >> lb) != blockIdx.x) continue;
             u32 hi = slink(sp, (u32)i, (u32)(w - b0));
-            if (hi != PG_INV) HAB[2 * (b0 + hi)] = make_uint2((u32)v, (u32)w);
+            if (hi != PG_INV) HookRec{HAB, NEXT ? HEAD : nullptr, NEXT}((u32)(b0 + hi), (u32)v, (u32)w);
         }
     }
     __syncthreads();
@@ -295,16 +295,16 @@ __device__ __forceinline__ void uf_find_lockstep(u32* P, u32 (&x)[K]) {
 }
 
 __device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restrict__ off,
-                                              const int32_t* __restrict__ tgt, u32* P, uint2* HAB);
+                                              const int32_t* __restrict__ tgt, u32* P, const HookRec& rec);
 __global__ void k_cc_sample(i64 n, int lb, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
-                            uint2* HAB, const u32* gate) {
+                            HookRec rec, const u32* gate) {
     const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n || gated_off(gate, 0)) return;
-    cc_sample_one(v, lb, off, tgt, P, HAB);
+    cc_sample_one(v, lb, off, tgt, P, rec);
 }
 
 __device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restrict__ off,
-                                              const int32_t* __restrict__ tgt, u32* P, uint2* HAB) {
+                                              const int32_t* __restrict__ tgt, u32* P, const HookRec& rec) {
     i64 a = off[v], b = off[v + 1];
     u32 t[NSAMPLE], x[NSAMPLE + 1];
     bool act[NSAMPLE], any = false;
@@ -326,7 +326,7 @@ __device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restri
     for (int k = 0; k < NSAMPLE; ++k) {
         if (!act[k]) continue;
         if (fallback) {
-            uf_link_hook(P, (u32)v, t[k], HAB);
+            uf_link_hook(P, (u32)v, t[k], rec);
             continue;
         }
         u32 rb = x[k + 1];
@@ -335,13 +335,13 @@ __device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restri
         if (rb == rv) continue;
         const u32 hi = rv > rb ? rv : rb, lo = rv ^ rb ^ hi;
         if (atomicCAS(P + hi, hi, lo) == hi) {
-            HAB[2 * (size_t)hi] = make_uint2((u32)v, t[k]);
+            rec(hi, (u32)v, t[k]);
             hooked[nh] = hi;
             under[nh] = lo;
             ++nh;
             rv = lo;
         } else {
-            uf_link_hook(P, (u32)v, t[k], HAB);
+            uf_link_hook(P, (u32)v, t[k], rec);
             fallback = true;
         }
     }
@@ -442,7 +442,7 @@ __device__ __forceinline__ void queue_heavy(i64 n, i64 len, u32 u, u32* heavy, u
     else heavy[atomicAdd(nh, 1u)] = u;
 }
 
-__global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+__global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, HookRec HAB,
                           Ctr* ctr, u32* heavy, const u32* gate) {
     const i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n || gated_off(gate, 0)) return;
@@ -457,7 +457,7 @@ __global__ void k_cc_rest(i64 n, const i64* __restrict__ off, const int32_t* __r
 
 template <int SKIP>
 __global__ void k_cc_rest_heavy(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P,
-                                uint2* HAB, const Ctr* ctr, const u32* __restrict__ heavy, const u32* gate, u32 want) {
+                                HookRec HAB, const Ctr* ctr, const u32* __restrict__ heavy, const u32* gate, u32 want) {
     if (gated_off(gate, want)) return;
     const u32 nh = ctr->nheavy, nvh = ctr->nvheavy;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
@@ -580,7 +580,7 @@ __device__ __forceinline__ void vgc_push_frontier(u32* FR, Ctr* ctr, bool push, 
 // expansions the queue is flushed to the frontier and the warp starts afresh.
 constexpr int VGC_K = 4;
 __global__ void __launch_bounds__(VGC_WARPS * 32, 8) k_vgc_search(i64 n, const i64* __restrict__ off,
-                                                               const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+                                                               const int32_t* __restrict__ tgt, u32* P, HookRec HAB,
                                                                u32* FR, Ctr* ctr, int tau, const u32* gate) {
     __shared__ uint2 qs[VGC_WARPS][VGC_Q];
     if (gated_off(gate, 1)) return;
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(VGC_WARPS * 32, 8) k_vgc_search(i64 n, const i
                     o[k] = atomicCAS(P + w[k], PG_INV, ss[k]);
                     if (o[k] == PG_INV) {
                         claimed[k] = true;
-                        HAB[2 * (size_t)w[k]] = make_uint2(su[k], w[k]);
+                        HAB(w[k], su[k], w[k]);
                     }
                 }
             }
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(VGC_WARPS * 32, 8) k_vgc_search(i64 n, const i
 
 // frontier rows: link every neighbour's tree (all vertices are claimed); long rows go to
 // the block-per-row list (k_cc_rest_heavy with skip 0)
-__global__ void k_vgc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, uint2* HAB,
+__global__ void k_vgc_rest(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, u32* P, HookRec HAB,
                            const u32* __restrict__ FR, Ctr* ctr, u32* heavy, const u32* gate) {
     if (gated_off(gate, 1)) return;
     const u32 nfr = ctr->nfr;
@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, const uint2* __res
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
             const u32 key = d ? e.y : e.x, arc = 2 * (u32)x + d;
+            if (key == (u32)x) continue;                    // own arc: placed when x was hooked (HookRec)
             u32 h = (key * 0x9E3779B1u) >> (32 - 12);     // AL_H = 2^12 slots
             for (;;) {
                 const u32 k = atomicCAS(hkey + h, PG_INV, key);
@@ -813,21 +814,6 @@ __global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, const uint2* __res
         if (key[j] != PG_INV) NEXT[htail[threadIdx.x + j * AL_T]] = old[j];
 }
 
-__global__ void k_arc_link(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
-    i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    uint2 e = x < n ? HAB[2 * x] : make_uint2(PG_INV, PG_INV);
-    const bool act = e.x != PG_INV;
-    const u32 arc_a = 2 * (u32)x, arc_b = 2 * (u32)x + 1;   // a->b out of a, b->a out of b
-    ArcGroup ga = arc_group(e.x, act, lane);
-    ArcGroup gb = arc_group(e.y, act, lane);
-    if (!act) return;
-    u32 olda = 0, oldb = 0;
-    if (lane == ga.lead) olda = atomicExch(HEAD + e.x, arc_a);
-    if (lane == gb.lead) oldb = atomicExch(HEAD + e.y, arc_b);
-    arc_splice(NEXT, ga, arc_a, olda);
-    arc_splice(NEXT, gb, arc_b, oldb);
-}
 
 // Close every out-arc list into a cycle (a root's cycle exits through its up arc).  Roots:
 //   isolated (no forest arc): preorder slot f from a warp-aggregated counter, written here;
@@ -2013,30 +1999,28 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     const int mode = cc_mode();
     const bool vgc_possible = mode == 1 || (mode == 0 && n >= VGC_MIN_N && m <= VGC_MAX_DEG * n);
     const u32* gate = vgc_possible ? &w.ctr->cc_vgc : nullptr;
+    const HookRec hook{w.HAB, w.HEAD, w.NEXT};
     const unsigned capped = (unsigned)(nblk(n, B) < 148 * 8 ? nblk(n, B) : 148 * 8);
     if (vgc_possible) {
         PG_K(k_cc_policy<<<1, POLICY_SAMPLES, 0, st>>>(n, m, off, tgt, seed, mode, w.ctr));
         PG_K(k_vgc_init<<<capped, B, 0, st>>>(n, off, w.P, w.HAB, w.HEAD, w.CROW, gate));
-        PG_K(k_vgc_search<<<vgc_grid(), VGC_WARPS * 32, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, vgc_tau(),
+        PG_K(k_vgc_search<<<vgc_grid(), VGC_WARPS * 32, 0, st>>>(n, off, tgt, w.P, hook, w.UOFF, w.ctr, vgc_tau(),
                                                                  gate));
-        PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.UOFF, w.ctr, w.HEAVY, gate));
-        PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 1));
+        PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, hook, w.UOFF, w.ctr, w.HEAVY, gate));
+        PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, hook, w.ctr, w.HEAVY, gate, 1));
     }
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.CROW,
-                                                                         gate));
-    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, gate));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.NEXT,
+                                                                         w.CROW, gate));
+    PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, hook, gate));
     PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, gate));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant, gate));
-    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate));
-    PG_K(k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, gate, 0));
+    PG_K(k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, hook, w.ctr, w.HEAVY, gate));
+    PG_K(k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, hook, w.ctr, w.HEAVY, gate, 0));
     // no final compress: later stages only ask "is x a root", and P[x] == x exactly at roots
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
-    if (getenv("PASGAL_BCC_ARC_WARP"))
-        PG_K(k_arc_link<<<nblk(n, B), B, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
-    else
-        PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
     PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
         n, w.HAB, w.HEAD, w.P, w.ctr, w.NEXT,
         IsoOut{w.FL, w.PV, w.E, w.PPAR, w.W, w.ROOTMARK}));
@@ -2209,13 +2193,14 @@ int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* w
     PG_CUDA_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(Ctr), st));
     if (n > 0) {
         const int lb = local_lb(n);
+        const HookRec rec{w.HAB, nullptr, nullptr};   // forest edges only: no out-arc lists here
         k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, nullptr,
-                                                                        nullptr);
-        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, nullptr);
+                                                                        nullptr, nullptr);
+        k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, rec, nullptr);
         k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, nullptr);
         k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant, nullptr);
-        k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, nullptr);
-        k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, w.HAB, w.ctr, w.HEAVY, nullptr, 0);
+        k_cc_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.P, rec, w.ctr, w.HEAVY, nullptr);
+        k_cc_rest_heavy<NSAMPLE><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, rec, w.ctr, w.HEAVY, nullptr, 0);
         k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, nullptr);
         k_cc_out<<<nblk(n, B), B, 0, st>>>(n, w.P, comp, w.ctr);
     }

@@ -93,15 +93,34 @@ __device__ __forceinline__ bool uf_link(u32* P, u32 a, u32 b) {
     return false;
 }
 
+// Where a hook is recorded: HAB[2 hi] = {a, b} (each vertex is hooked at most once, so
+// HAB names a spanning forest).  When the edge leaves hi itself (a == hi: arc 2hi; b == hi:
+// arc 2hi+1) that "own" arc is also made the first entry of hi's out-arc list (HEAD[hi],
+// NEXT[arc] = end) right here -- nothing else touches hi's list before the forest stage --
+// so the forest stage's list building only inserts the other arcs (fewer returning
+// exchanges).  HEAD == nullptr records the edge only.
+struct HookRec {
+    uint2* HAB;
+    u32* HEAD;
+    u32* NEXT;
+    __device__ __forceinline__ void operator()(u32 hi, u32 a, u32 b) const {
+        HAB[2 * (size_t)hi] = make_uint2(a, b);
+        if (HEAD && (a == hi || b == hi)) {
+            const u32 own = 2 * hi + (a == hi ? 0u : 1u);
+            NEXT[own] = PG_INV;
+            HEAD[hi] = own;
+        }
+    }
+};
+
 // link a-b and record the graph edge that caused the merge at the hooked root
-// (HAB[2 hi] = {a, b}; each vertex is hooked at most once, so HAB names a spanning forest)
-__device__ __forceinline__ void uf_link_hook(u32* P, u32 a, u32 b, uint2* HAB) {
+__device__ __forceinline__ void uf_link_hook(u32* P, u32 a, u32 b, const HookRec& rec) {
     u32 ra = uf_find(P, a), rb = uf_find(P, b);
     while (ra != rb) {
         u32 hi = ra > rb ? ra : rb, lo = ra ^ rb ^ hi;
         u32 old = atomicCAS(P + hi, hi, lo);
         if (old == hi) {
-            HAB[2 * (size_t)hi] = make_uint2(a, b);
+            rec(hi, a, b);
             return;
         }
         ra = uf_find(P, ra);
