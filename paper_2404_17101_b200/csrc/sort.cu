@@ -139,7 +139,15 @@ struct OsPass {
 struct OsPasses {
     OsPass p[OS_MAXP];
     int np;
+    int vb;
 };
+
+// The bits that vary, packed: row bits [32, 32+vb) above column bits [0, vb), so a
+// 2vb-bit key takes ceil(2vb/8) passes (C5a: 7, not 2 x 4).  The all-ones sentinel packs to
+// all ones and sorts last.
+__device__ __forceinline__ u64 os_vkey(u64 k, int vb) {
+    return ((k >> 32) << vb) | (k & ((1ull << vb) - 1));
+}
 
 // per-warp shared-memory histograms (plain shared atomics: a power-law graph's hub digits
 // collide, and a match_any per key and pass ran at 230 GB/s), merged per block
@@ -161,7 +169,8 @@ __global__ void __launch_bounds__(OSH_T) k_os_hist(const u64* __restrict__ keys,
             if (base + j < nkeys) {
 #pragma unroll
                 for (int q = 0; q < OS_MAXP; ++q)
-                    if (q < np) atomicAdd(h + q * RS_BINS + ((u32)(k[j] >> ps.p[q].shift) & ps.p[q].mask), 1u);
+                    if (q < np)
+                        atomicAdd(h + q * RS_BINS + ((u32)(os_vkey(k[j], ps.vb) >> ps.p[q].shift) & ps.p[q].mask), 1u);
             }
     }
     __syncthreads();
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(RS_BINS) k_os_goff(int np, const unsigned long
 }
 
 __global__ void __launch_bounds__(OS_T, PG_OS_MINB) k_os_pass(const u64* __restrict__ in, u64* __restrict__ out, i64 nkeys,
-                                                  int shift, u32 mask, u32 epoch, const u64* __restrict__ GOFF,
+                                                  int vb, int shift, u32 mask, u32 epoch, const u64* __restrict__ GOFF,
                                                   u64* status, u32* tile_ctr) {
     extern __shared__ __align__(16) unsigned char os_smem[];
     u64* sk = (u64*)os_smem;                                  // [OS_TILE] keys, digit-sorted
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(OS_T, PG_OS_MINB) k_os_pass(const u64* __restr
         const i64 i = seg + 32 * j + lane;
         const bool valid = i < nkeys;
         const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
-        const u32 d = (u32)(k[j] >> shift) & mask;
+        const u32 d = (u32)(os_vkey(k[j], vb) >> shift) & mask;
         unsigned peers = 0;
         u32 before = 0;
         if (valid) {
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(OS_T, PG_OS_MINB) k_os_pass(const u64* __restr
     for (int j = 0; j < OS_ITEMS; ++j) {
         const i64 i = seg + 32 * j + lane;
         if (i < nkeys) {
-            const u32 d = (u32)(k[j] >> shift) & mask;
+            const u32 d = (u32)(os_vkey(k[j], vb) >> shift) & mask;
             sk[tb[d] + wc[w * RS_BINS + d] + r[j]] = k[j];
         }
     }
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(OS_T, PG_OS_MINB) k_os_pass(const u64* __restr
     const i64 tcount = nkeys - t0 < OS_TILE ? nkeys - t0 : OS_TILE;
     for (int q = threadIdx.x; q < tcount; q += OS_T) {
         const u64 key = sk[q];
-        const u32 d = (u32)(key >> shift) & mask;
+        const u32 d = (u32)(os_vkey(key, vb) >> shift) & mask;
         out[gb[d] + (u64)(q - tb[d])] = key;
     }
 }
@@ -313,11 +322,11 @@ static cudaError_t onesweep_sort(u64* keys, u64* alt, i64 nkeys, int vb, void* t
     *result = keys;
     if (nkeys <= 1) return cudaSuccess;
     OsPasses ps{};
-    for (int part = 0; part < 2; ++part)
-        for (int bit = 0; bit < vb; bit += 8) {
-            const int width = vb - bit < 8 ? vb - bit : 8;
-            ps.p[ps.np++] = OsPass{(part ? 32 : 0) + bit, (1u << width) - 1u};
-        }
+    ps.vb = vb;
+    for (int bit = 0; bit < 2 * vb; bit += 8) {
+        const int width = 2 * vb - bit < 8 ? 2 * vb - bit : 8;
+        ps.p[ps.np++] = OsPass{bit, (1u << width) - 1u};
+    }
     char* t = (char*)temp;
     unsigned long long* G = (unsigned long long*)t;
     t += al256(8 * (size_t)OS_MAXP * RS_BINS);
@@ -352,7 +361,7 @@ static cudaError_t onesweep_sort(u64* keys, u64* alt, i64 nkeys, int vb, void* t
     }
     u64 *src = keys, *dst = alt;
     for (int q = 0; q < ps.np; ++q) {
-        k_os_pass<<<(unsigned)ntiles, OS_T, OS_SMEM, st>>>(src, dst, nkeys, ps.p[q].shift, ps.p[q].mask, (u32)(q + 1),
+        k_os_pass<<<(unsigned)ntiles, OS_T, OS_SMEM, st>>>(src, dst, nkeys, vb, ps.p[q].shift, ps.p[q].mask, (u32)(q + 1),
                                                            GOFF + q * RS_BINS, status, ctr + q);
         u64* tmp = src;
         src = dst;
