@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cub/block/block_reduce.cuh>
+#include <nvtx3/nvToolsExt.h>
 #include "common.cuh"
 #include "scan.cuh"
 #include "wchunk.cuh"
@@ -1952,7 +1953,21 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     const int32_t* tgt = g->targets;
     const int B = 256;
     int nl = 0;  // kernel launches issued by this call
+    // stage boundaries: the caller's CUDA events, and NVTX ranges named after the stages
+    // (host launch intervals in nsys / ncu --nvtx; no cost without an attached tool)
+    static const char* const stage_names[PASGAL_BCC_NSTAGES] = {
+        "pasgal_bcc", "first_cc", "forest", "listrank", "tour", "tags", "rmq", "last_cc", "artic", "labels",
+        "canonical"};
+    int nvtx_open = 0;
     auto mark = [&](int stage) -> cudaError_t {
+        if (nvtx_open) {
+            nvtxRangePop();
+            nvtx_open = 0;
+        }
+        if (stage + 1 < PASGAL_BCC_NSTAGES) {
+            nvtxRangePushA(stage_names[stage + 1]);
+            nvtx_open = 1;
+        }
         if (prof && prof->events && stage < prof->n_events && prof->events[stage])
             return cudaEventRecord((cudaEvent_t)prof->events[stage], st);
         return cudaSuccess;
