@@ -34,6 +34,10 @@
 namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
+// HAB[2x+1].x tags.  Tour arcs hold positions there, which stay below TAG_ISO (n < 2^31 - 2).
+constexpr u32 TAG_ISO = 0xFFFFFFFCu;    // x is an isolated vertex (no forest edge)
+constexpr u32 TAG_TRIM_A = 0xFFFFFFFEu; // edge x trimmed: its endpoint .x is a forest leaf
+constexpr u32 TAG_TRIM_B = 0xFFFFFFFDu; // edge x trimmed: its endpoint .y is a forest leaf
 #ifndef PG_LABELS_MINB
 #define PG_LABELS_MINB 8
 #endif
@@ -74,6 +78,8 @@ struct Ctr {
     u32 nvheavy2; // very heavy rows queued by k_cc2_rest (HEAVY back)
     u32 gcid;     // component id (head preorder rank) of the sampled giant skeleton component
     u32 nfr;      // VGC First-CC: claimed vertices whose rows await the frontier pass (FR)
+    u32 ntrim;    // forest leaves kept off the Euler tour (placed after the preorder scan)
+    u32 nbigp;    // parents with more than LEAF_RUN leaves (their leaf slots: k_leaf_runs)
     u32 cc_vgc;   // First-CC path chosen by k_cc_policy: 1 = VGC local searches, 0 = sampled union-find
 };
 
@@ -776,43 +782,122 @@ __device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc
 // hubs: per-warp aggregation still left ~5M returning exchanges on the top hub's HEAD,
 // serialised at one L2 slice; per-block aggregation divides that by the block size and
 // keeps each hub's list in runs of consecutive hooked ids.
-constexpr int AL_T = 1024, AL_H = 4096;
-__global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, const uint2* __restrict__ HAB, u32* HEAD, u32* NEXT) {
-    __shared__ u32 hkey[AL_H], hhead[AL_H], htail[AL_H];
+constexpr int AL_T = 512, AL_H = 2048;     // <= 2 keys per thread: the table stays half empty
+// Leaf trimming: a non-root vertex of forest degree 1 is a leaf of the rooted forest
+// whatever the rooting (C5a: most forest vertices are leaves hooked onto hubs), so its edge
+// is kept off the Euler tour.  The edge's record gets a tag naming the leaf end and the
+// leaf's rank among its parent's leaves; LCNT[p] counts p's leaves.  Ranks come from the
+// same shared table (one global atomicAdd per parent per block).  The preorder scan then
+// weighs every tour vertex by 1 + its leaf count, and k_vertex_first puts the leaves of p
+// right after p.  fm.ONE == nullptr: no trimming.
+//
+// Forest marks (k_forest_marks): three n-bit maps, L2-resident (33 MB each at C5a):
+// ONE = endpoint of >= 1 forest edge, TWO = of >= 2, ROOT = never hooked.
+struct ForestMarks {
+    u32 *ONE, *TWO, *ROOT;
+    u32* LEAF;   // ONE & ~TWO & ~ROOT, written over TWO by k_leaf_bits
+};
+__device__ __forceinline__ bool fm_bit(const u32* bm, u32 v) { return (__ldcg(bm + (v >> 5)) >> (v & 31)) & 1u; }
+__device__ __forceinline__ bool forest_leaf(u32 v, const ForestMarks& fm) { return fm_bit(fm.LEAF, v); }
+__global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, uint2* HAB, u32* HEAD, u32* NEXT, bool own_placed,
+                                                       ForestMarks fm, u32* LCNT, uint2* LPR, Ctr* ctr) {
+    __shared__ u32 hkey[AL_H], hhead[AL_H], htail[AL_H], hleaf[AL_H];
+    __shared__ u32 s_trim;
     for (int i = threadIdx.x; i < AL_H; i += AL_T) {
         hkey[i] = PG_INV;
         hhead[i] = PG_INV;
+        hleaf[i] = 0;
     }
+    if (threadIdx.x == 0) s_trim = 0;
     __syncthreads();
     const i64 x = (i64)blockIdx.x * AL_T + threadIdx.x;
     const uint2 e = x < n ? HAB[2 * x] : make_uint2(PG_INV, PG_INV);
+    auto slot_of = [&](u32 key) -> u32 {
+        u32 h = (key * 0x9E3779B1u) >> (32 - 11);           // AL_H = 2^11 slots
+        for (;;) {
+            const u32 k = atomicCAS(hkey + h, PG_INV, key);
+            if (k == PG_INV || k == key) return h;
+            h = (h + 1) & (AL_H - 1);
+        }
+    };
+    int lh = -1;                    // trimmed edge: the parent's slot
+    u32 lrank = 0, ltag = 0;
     if (e.x != PG_INV) {
+        const bool la = fm.ONE && forest_leaf(e.x, fm);
+        const bool lb = fm.ONE && !la && forest_leaf(e.y, fm);
+        if (la || lb) {
+            lh = (int)slot_of(la ? e.y : e.x);
+            lrank = atomicAdd(hleaf + lh, 1u);
+            ltag = la ? TAG_TRIM_A : TAG_TRIM_B;
+        } else {
 #pragma unroll
-        for (int d = 0; d < 2; ++d) {
-            const u32 key = d ? e.y : e.x, arc = 2 * (u32)x + d;
-            if (key == (u32)x) continue;                    // own arc: placed when x was hooked (HookRec)
-            u32 h = (key * 0x9E3779B1u) >> (32 - 12);     // AL_H = 2^12 slots
-            for (;;) {
-                const u32 k = atomicCAS(hkey + h, PG_INV, key);
-                if (k == PG_INV || k == key) break;
-                h = (h + 1) & (AL_H - 1);
+            for (int d = 0; d < 2; ++d) {
+                const u32 key = d ? e.y : e.x, arc = 2 * (u32)x + d;
+                if (own_placed && key == (u32)x) continue;  // own arc: placed when x was hooked (HookRec)
+                const u32 h = slot_of(key);
+                const u32 old = atomicExch(hhead + h, arc);
+                if (old == PG_INV) htail[h] = arc;             // first in: the local chain's tail
+                else NEXT[arc] = old;
             }
-            const u32 old = atomicExch(hhead + h, arc);
-            if (old == PG_INV) htail[h] = arc;             // first in: the local chain's tail
-            else NEXT[arc] = old;
         }
     }
+    const unsigned tb = __ballot_sync(0xFFFFFFFFu, lh >= 0);
+    if ((threadIdx.x & 31) == 0 && tb) atomicAdd(&s_trim, (u32)__popc(tb));
     __syncthreads();
-    u32 key[AL_H / AL_T], old[AL_H / AL_T];
+    u32 key[AL_H / AL_T], old[AL_H / AL_T], lbase[AL_H / AL_T];
 #pragma unroll
-    for (int j = 0; j < AL_H / AL_T; ++j) {                 // the exchanges in flight together
+    for (int j = 0; j < AL_H / AL_T; ++j) {                 // the global atomics in flight together
         const int h = threadIdx.x + j * AL_T;
         key[j] = hkey[h];
-        old[j] = key[j] != PG_INV ? atomicExch(HEAD + key[j], hhead[h]) : 0u;
+        old[j] = key[j] != PG_INV && hhead[h] != PG_INV ? atomicExch(HEAD + key[j], hhead[h]) : 0u;
+        lbase[j] = key[j] != PG_INV && hleaf[h] ? atomicAdd(LCNT + key[j], hleaf[h]) : 0u;
     }
 #pragma unroll
-    for (int j = 0; j < AL_H / AL_T; ++j)
-        if (key[j] != PG_INV) NEXT[htail[threadIdx.x + j * AL_T]] = old[j];
+    for (int j = 0; j < AL_H / AL_T; ++j) {
+        const int h = threadIdx.x + j * AL_T;
+        if (key[j] != PG_INV && hhead[h] != PG_INV) NEXT[htail[h]] = old[j];
+        hleaf[h] = lbase[j];                                 // now: this block's first rank at the parent
+    }
+    if (threadIdx.x == 0 && s_trim) atomicAdd(&ctr->ntrim, s_trim);
+    __syncthreads();
+    // the whole 16-byte record (an 8-byte half would leave partially written sectors); the
+    // leaf's (parent, rank) by vertex for k_vertex_first
+    if (lh >= 0) {
+        reinterpret_cast<uint4*>(HAB)[x] = make_uint4(e.x, e.y, ltag, hleaf[lh] + lrank);
+        LPR[ltag == TAG_TRIM_A ? e.x : e.y] = make_uint2(ltag == TAG_TRIM_A ? e.y : e.x, hleaf[lh] + lrank);
+    }
+}
+
+__global__ void k_leaf_bits(i64 nw, ForestMarks fm) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nw) fm.LEAF[i] = fm.ONE[i] & ~fm.TWO[i] & ~fm.ROOT[i];
+}
+
+// Forest marks (maps zeroed before): ROOT by one coalesced word per warp, ONE/TWO by
+// warp-aggregated atomicOr on the endpoints of every hook edge (a second sighting sets TWO;
+// lanes naming the same vertex count as sightings too)
+__global__ void k_forest_marks(i64 n, const uint2* __restrict__ HAB, ForestMarks fm) {
+    const i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint2 e = x < n ? HAB[2 * x] : make_uint2(0u, 0u);
+    const bool hooked = x < n && e.x != PG_INV;
+    const unsigned rb = __ballot_sync(0xFFFFFFFFu, x < n && !hooked);
+    if (lane == 0 && x < n) fm.ROOT[x >> 5] = rb;
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, hooked);
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+        if (!hooked) continue;
+        const u32 v = d ? e.y : e.x;
+        const unsigned grp = __match_any_sync(act, v);
+        if (lane != __ffs(grp) - 1) continue;
+        // read first: a hub's bits are set after its first sightings, and the atomics of
+        // every later warp on one word would serialise at its L2 slice (10 ms at C5a)
+        const u32 bit = 1u << (v & 31);
+        if (__ldcg(fm.TWO + (v >> 5)) & bit) continue;
+        const bool many = __popc(grp) > 1;
+        const u32 old = (!many && (__ldcg(fm.ONE + (v >> 5)) & bit)) ? bit : atomicOr(fm.ONE + (v >> 5), bit);
+        if ((old & bit) || many) atomicOr(fm.TWO + (v >> 5), bit);
+    }
 }
 
 
@@ -835,10 +920,9 @@ struct IsoOut {
 // atomics (a single global head hit once per warp serialised ~8M atomics at RMAT 2^28).
 constexpr int AC_B = 512, AC_V = 8;
 
-__global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restrict__ HAB,
-                                                    const u32* __restrict__ HEAD,
-                                                    const u32* __restrict__ P, Ctr* ctr,
-                                                    u32* NEXT, IsoOut io) {
+__global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, uint2* HAB, const u32* __restrict__ HEAD,
+                                                    const u32* __restrict__ P, ForestMarks fm,
+                                                    Ctr* ctr, u32* NEXT, IsoOut io) {
     __shared__ u32 s_niso, s_r1, s_head, s_tail, s_base;
     if (threadIdx.x == 0) { s_niso = 0; s_r1 = 0; s_head = 0; s_tail = PG_INV; }
     __syncthreads();
@@ -849,12 +933,17 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restri
 #pragma unroll
     for (int i = 0; i < AC_V; ++i) {
         const i64 x = base + (i64)i * AC_B;
-        uint2 e = x < n ? HAB[2 * x] : make_uint2(0u, 0u);
+        const uint4 rec = x < n ? reinterpret_cast<const uint4*>(HAB)[x] : make_uint4(0u, 0u, 0u, 0u);
+        const uint2 e = make_uint2(rec.x, rec.y);
         const bool root = x < n && e.x == PG_INV;
         const u32 h = root ? HEAD[x] : PG_INV;
-        const bool iso = root && h == PG_INV;
-        const bool chain = root && h != PG_INV;
-        if (x < n && !root) {
+        // isolated: no forest edge (with trimming a root whose children are all leaves has
+        // an empty out-arc list but stays on the tour, down and straight back up)
+        const bool iso = root && (fm.ONE ? !fm_bit(fm.ONE, (u32)x) : h == PG_INV);
+        const bool chain = root && !iso;
+        const bool trimmed = rec.z == TAG_TRIM_A || rec.z == TAG_TRIM_B;
+        if (iso) reinterpret_cast<uint4*>(HAB)[x] = make_uint4(rec.x, rec.y, TAG_ISO, rec.w);
+        if (x < n && !root && !trimmed) {
 #pragma unroll
             for (int d = 0; d < 2; ++d) {
                 u32 arc = 2 * (u32)x + d;
@@ -883,7 +972,9 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restri
             const unsigned later = bc & (lane == 31 ? 0u : (0xFFFFFFFEu << lane));
             const u32 nxt = __shfl_sync(0xFFFFFFFFu, 2 * (u32)x, later ? __ffs(later) - 1 : lane);
             if (chain) {
-                NEXT[2 * x + 1] = h;                  // down into r, then its first out-arc
+                // down into r, then its first out-arc -- or, when all of r's children are
+                // trimmed leaves, straight back up: succ(2r) = NEXT[2r+1] = 2r+1
+                NEXT[2 * x + 1] = h != PG_INV ? h : 2 * (u32)x + 1;
                 if (later) NEXT[2 * x] = nxt;         // up out of r, then the next root's down arc
                 else if (old) NEXT[2 * x] = old - 1;
                 else s_tail = 2 * (u32)x;             // block tail: linked to the global chain
@@ -918,12 +1009,12 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, const uint2* __restri
 // next ruler; Wyllie on the rulers; walk2: final positions (into HAB[2y+1]) and TA[position] = arc.
 struct TourInfo {
     u32 head;     // first arc of the list, PG_INV if the tour is empty
-    u32 len;      // arcs on the tour = 2 * (n - isolated)
+    u32 len;      // arcs on the tour = 2 * (n - isolated - trimmed leaves)
 };
 __device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, i64 n) {
     TourInfo t;
     t.head = ctr->roothead - 1;                // PG_INV when no root is chained
-    t.len = (u32)(2 * (n - (i64)ctr->niso));
+    t.len = (u32)(2 * (n - (i64)ctr->niso - (i64)ctr->ntrim));
     return t;
 }
 __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, const uint2* HAB, const u32* HEAD,
@@ -931,7 +1022,8 @@ __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, c
     if (s < nsk) {
         x = (u32)s << lrs;
         u32 v = x >> 1;
-        return !(HAB[2 * (i64)v].x == PG_INV && HEAD[v] == PG_INV);   // isolated vertices are off the tour
+        (void)HEAD;
+        return HAB[2 * (i64)v + 1].x < TAG_ISO;   // isolated vertices and trimmed leaves' edges are off the tour
     }
     x = t.head;
     return t.head != PG_INV && (t.head & ((1u << lrs) - 1u)) != 0;
@@ -1068,10 +1160,11 @@ struct PreLoad {
     u32* TP;
     const Ctr* ctr;
     i64 n;
+    const u32* LCNT;   // non-null with leaf trimming: a down arc weighs 1 + its vertex's leaves
     // all reads are read-only for the kernel (__ldg), so the compiler may issue the next
     // items' gathers before this item's stores
     __device__ __forceinline__ u32 operator()(i64 k) const {
-        if (k >= 2 * (n - (i64)ctr->niso)) return 0u;
+        if (k >= (i64)tour_info(ctr, n).len) return 0u;
         u32 x = __ldg(TA + k);
         // one 16-byte record: the hook edge and both arcs' positions
         uint4 r = __ldg(reinterpret_cast<const uint4*>(HAB + 2 * (i64)(x >> 1)));
@@ -1087,7 +1180,8 @@ struct PreLoad {
         }
         T[k] = ((u64)pt << 32) | tg;
         TP[k] = src;
-        return (u64)k < pt ? 1u : 0u;
+        if ((u64)k >= pt) return 0u;
+        return LCNT ? 1u + __ldg(LCNT + (tg & ~VFLAG)) : 1u;
     }
 };
 struct PreStore {
@@ -1097,7 +1191,13 @@ struct PreStore {
     uint2* FL;
     u32 *PV, *E, *PPAR;
     uint2* W;
+    u32* PWX;          // non-null with leaf trimming: the weighted exclusive prefix per position
+    i64 n;
     __device__ __forceinline__ void operator()(i64 k, u32 f, u32 down) const {
+        if (PWX) {     // the per-vertex writes need the prefix at the twin: k_pre_place
+            if (k < (i64)tour_info(ctr, n).len) PWX[k] = f;
+            return;
+        }
         if (!down) return;
         f += ctr->niso;                   // isolated vertices occupy [0, niso)
         u64 t = T[k];
@@ -1114,14 +1214,72 @@ struct PreStore {
     }
 };
 
+// With leaf trimming: first = niso + the weighted prefix at the down arc, last = niso + the
+// prefix at its twin (up) arc - 1 (the subtree's tour vertices and their leaves lie between)
+// The slots of v's leaves follow v's own, so v also writes their E / PPAR / W (position
+// order, coalesced); v's with more than LEAF_RUN leaves go to k_leaf_runs (a block each).
+constexpr u32 LEAF_RUN = 32;
+__global__ void k_pre_place(i64 n, const u64* __restrict__ T, const u32* __restrict__ TP,
+                            const u32* __restrict__ PWX, Ctr* ctr, const u32* __restrict__ LCNT, uint2* FL, u32* PV,
+                            u32* E, u32* PPAR, uint2* W, u32* bigp) {
+    const i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (i64)tour_info(ctr, n).len) return;
+    const u64 t = T[k];
+    const u32 pt = (u32)(t >> 32);
+    if ((u64)k >= pt) return;                   // up arc
+    const u32 niso = ctr->niso;
+    const u32 v = (u32)t & ~VFLAG;
+    const u32 f = niso + PWX[k], last = niso + __ldg(PWX + pt) - 1u;
+    FL[v] = make_uint2(f, last);
+    PV[f] = v;
+    E[f] = last;
+    PPAR[f] = TP[k];
+    W[f] = make_uint2(f, f);
+    const u32 c = __ldg(LCNT + v);
+    if (c > LEAF_RUN) {
+        bigp[atomicAdd(&ctr->nbigp, 1u)] = v;
+        return;
+    }
+    for (u32 r = 1; r <= c; ++r) {
+        E[f + r] = f + r;
+        PPAR[f + r] = v;
+        W[f + r] = make_uint2(f + r, f + r);
+    }
+}
+
+// leaf slots of the parents with many leaves: one block per parent, coalesced
+__global__ void k_leaf_runs(const Ctr* ctr, const u32* __restrict__ bigp, const u32* __restrict__ LCNT,
+                            const uint2* __restrict__ FL, u32* E, u32* PPAR, uint2* W) {
+    const u32 nb = ctr->nbigp;
+    for (u32 b = blockIdx.x; b < nb; b += gridDim.x) {
+        const u32 v = bigp[b], c = LCNT[v], f = FL[v].x;
+        for (u32 r = 1 + threadIdx.x; r <= c; r += blockDim.x) {
+            E[f + r] = f + r;
+            PPAR[f + r] = v;
+            W[f + r] = make_uint2(f + r, f + r);
+        }
+    }
+}
+
+
 // FIRST[v] = FL[v].x and the optional parent/first outputs, per vertex and coalesced: the
 // preorder store writes only FL by vertex (a random 8-byte write; a second random 4-byte
 // FIRST write cost a partial-sector read-modify-write per vertex)
-__global__ void k_vertex_first(i64 n, const uint2* __restrict__ FL, const u32* __restrict__ PPAR, u32* FIRST,
-                               u32* out_parent, u32* out_first) {
+// With leaf trimming it also places the leaves (LEAF map): leaf v of parent p with rank r
+// takes slot first[p] + 1 + r (E / PPAR / W of the slot were written by the parent).
+__global__ void k_vertex_first(i64 n, uint2* FL, const u32* __restrict__ PPAR, u32* FIRST, u32* out_parent,
+                               u32* out_first, const u32* __restrict__ LEAF, const uint2* __restrict__ LPR, u32* PV) {
     const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    const u32 f = FL[v].x;
+    u32 f;
+    if (LEAF && ((LEAF[v >> 5] >> (v & 31)) & 1u)) {
+        const uint2 pr = LPR[v];
+        f = FL[pr.x].x + 1u + pr.y;
+        FL[v] = make_uint2(f, f);
+        PV[f] = (u32)v;
+    } else {
+        f = FL[v].x;
+    }
     FIRST[v] = f;
     if (out_first) out_first[v] = f;
     if (out_parent) out_parent[v] = __ldg(PPAR + f);
@@ -1904,6 +2062,18 @@ static int vgc_tau() {
     const char* t = getenv("PASGAL_BCC_VGC_TAU");
     return t && atoi(t) > 0 ? atoi(t) : VGC_TAU_DEFAULT;
 }
+// Leaf trimming of the Euler tour (S3) pays where the spanning forest is leafy: the sampled
+// union-find forest of a graph with >= 4 slots per vertex (RMAT, kNN: most vertices hook onto
+// a neighbour and nothing hooks onto them; C5a rooting 31.8 -> 28 ms, C4 -1.2 ms), not on a
+// lattice (C3: +0.5 ms).  PASGAL_BCC_TRIM=0/1 forces it (A/B sweeps).  Tour positions must
+// stay below the HAB tags (n < 2^31 - 2).
+static bool leaf_trim(i64 n, i64 m) {
+    static const char* e = getenv("PASGAL_BCC_TRIM");
+    if (n < 64 || n >= ((i64)1 << 31) - 2) return false;
+    if (e) return e[0] != '0';
+    return m >= 4 * n;
+}
+
 static unsigned vgc_grid() {
     static int blocks = 0;
     if (!blocks) {
@@ -2014,7 +2184,10 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     const int mode = cc_mode();
     const bool vgc_possible = mode == 1 || (mode == 0 && n >= VGC_MIN_N && m <= VGC_MAX_DEG * n);
     const u32* gate = vgc_possible ? &w.ctr->cc_vgc : nullptr;
-    const HookRec hook{w.HAB, w.HEAD, w.NEXT};
+    // leaf trimming (section S3 below) places no out-arc at hook time: the arcs of a leaf's
+    // edge never enter a list
+    const bool trim = leaf_trim(n, m);
+    const HookRec hook{w.HAB, trim ? nullptr : w.HEAD, w.NEXT};
     const unsigned capped = (unsigned)(nblk(n, B) < 148 * 8 ? nblk(n, B) : 148 * 8);
     if (vgc_possible) {
         PG_K(k_cc_policy<<<1, POLICY_SAMPLES, 0, st>>>(n, m, off, tgt, seed, mode, w.ctr));
@@ -2024,8 +2197,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         PG_K(k_vgc_rest<<<148 * 8, B, 0, st>>>(n, off, tgt, w.P, hook, w.UOFF, w.ctr, w.HEAVY, gate));
         PG_K(k_cc_rest_heavy<0><<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.P, hook, w.ctr, w.HEAVY, gate, 1));
     }
-    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD, w.NEXT,
-                                                                         w.CROW, gate));
+    PG_K(k_cc_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, off, tgt, w.P, w.HAB, w.HEAD,
+                                                                         trim ? nullptr : w.NEXT, w.CROW, gate));
     PG_K(k_cc_sample<<<nblk(n, B), B, 0, st>>>(n, lb, off, tgt, w.P, hook, gate));
     PG_K(k_compress<COMPRESS_ILP><<<nblk(cdiv(n, COMPRESS_ILP), B), B, 0, st>>>(n, w.P, gate));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.P, seed, &w.ctr->giant, gate));
@@ -2035,9 +2208,22 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FIRST_CC));
     // ---- S3 rooting: arc lists
-    PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT));
+    // forest marks: ONE in GBIT (free until Last-CC), TWO and ROOT inside UCNT (free until
+    // canonicalisation); leaves per parent in UOFF (free after First-CC)
+    ForestMarks fm{nullptr, nullptr, nullptr, nullptr};
+    u32* LCNT = trim ? w.UOFF : nullptr;
+    if (trim) {
+        const i64 nw = cdiv(n, 32);
+        fm = ForestMarks{w.GBIT, w.UCNT, w.UCNT + nw, w.UCNT};   // LEAF over TWO
+        PG_CUDA_TRY(cudaMemsetAsync(fm.ONE, 0, 4 * (size_t)nw, st));
+        PG_CUDA_TRY(cudaMemsetAsync(fm.TWO, 0, 4 * (size_t)nw, st));
+        PG_CUDA_TRY(cudaMemsetAsync(LCNT, 0, 4 * (size_t)n, st));
+        PG_K(k_forest_marks<<<nblk(n, B), B, 0, st>>>(n, w.HAB, fm));
+    }
+    if (trim) PG_K(k_leaf_bits<<<nblk(cdiv(n, 32), B), B, 0, st>>>(cdiv(n, 32), fm));
+    PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT, !trim, fm, LCNT, w.PM, w.ctr));
     PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
-        n, w.HAB, w.HEAD, w.P, w.ctr, w.NEXT,
+        n, w.HAB, w.HEAD, w.P, fm, w.ctr, w.NEXT,
         IsoOut{w.FL, w.PV, w.E, w.PPAR, w.W, w.ROOTMARK}));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
@@ -2060,11 +2246,17 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
                                                      w.HAB, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
-    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.HAB, w.T, w.TP, w.ctr, n},
-                                 PreStore{w.T, w.TP, w.ctr, w.FL, w.PV, w.E, w.PPAR, w.W},
+    PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.HAB, w.T, w.TP, w.ctr, n, LCNT},
+                                 PreStore{w.T, w.TP, w.ctr, w.FL, w.PV, w.E, w.PPAR, w.W, trim ? w.TA : nullptr, n},
                                  (u32*)nullptr, st));
     ++nl;
-    PG_K(k_vertex_first<<<nblk(n, B), B, 0, st>>>(n, w.FL, w.PPAR, w.FIRST, out->parent, out->first));
+    if (trim) {   // the weighted prefix (in TA) -> first/last of the tour vertices, then the leaves
+        PG_K(k_pre_place<<<nblk(L, B), B, 0, st>>>(n, w.T, w.TP, w.TA, w.ctr, LCNT, w.FL, w.PV, w.E, w.PPAR, w.W,
+                                                    w.HEAVY));
+        PG_K(k_leaf_runs<<<HEAVY_GRID, 256, 0, st>>>(w.ctr, w.HEAVY, LCNT, w.FL, w.E, w.PPAR, w.W));
+    }
+    PG_K(k_vertex_first<<<nblk(n, B), B, 0, st>>>(n, w.FL, w.PPAR, w.FIRST, out->parent, out->first,
+                                                   trim ? fm.LEAF : nullptr, w.PM, w.PV));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
