@@ -285,6 +285,13 @@ int pasgal_msbfs_ex(const pasgal_csr_t* g, const int64_t* sources, int nsources,
 size_t pasgal_bfs_vgc_workspace_bytes(int64_t n);
 int pasgal_bfs_vgc(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* workspace,
                    size_t workspace_bytes, void* stream);
+/* pasgal_bfs_vgc with dense rounds (SPEC.md bfs_round_dense): when the graph is symmetric
+ * (`symmetric` != 0, the caller's promise) and the frontier's out-degree sum exceeds
+ * dense_threshold * m_slots, a round is taken bottom-up (every vertex scans its row for
+ * frontier members); identical distances.  *dense_rounds (host, nullable) counts them. */
+int pasgal_bfs_vgc_ex(const pasgal_csr_t* g, int64_t source, int tau, double dense_threshold, int symmetric,
+                      int32_t* dist, int64_t* rounds, int64_t* dense_rounds, void* workspace, size_t workspace_bytes,
+                      void* stream);
 
 /* Articulation bitmap -> one byte per vertex (0/1), on the device: the reference's
  * BccLabels.articulation bool[n] (results.py:45-88) without a host-side bit unpack.

@@ -81,6 +81,8 @@ SIGNATURES = {
     "pasgal_bfs_vgc_workspace_bytes": (_SZ, [_I64]),
     "pasgal_bfs_vgc": (_INT, [ctypes.POINTER(PasgalCsr), _I64, _INT, _VP, ctypes.POINTER(ctypes.c_int64), _VP, _SZ,
                               _VP]),
+    "pasgal_bfs_vgc_ex": (_INT, [ctypes.POINTER(PasgalCsr), _I64, _INT, ctypes.c_double, _INT, _VP,
+                                 ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), _VP, _SZ, _VP]),
     "pasgal_adj_temp_bytes": (_SZ, [_I64]),
     "pasgal_msbfs_workspace_bytes": (_SZ, [_I64]),
     "pasgal_msbfs": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(ctypes.c_int64), _INT, _VP,

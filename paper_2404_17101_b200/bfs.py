@@ -97,8 +97,9 @@ def bfs(g, source, device="cuda"):
 class VgcConfig:
     """SPEC.md vgc-engine VgcConfig: ``tau`` = minimum vertices a local search processes
     (>= 1), ``max_local_queue`` = its working-set cap (>= tau; the device queue holds 256
-    vertices per warp and overflows to the next frontier), ``dense_threshold`` kept for
-    interface parity (the device engine runs top-down rounds only)."""
+    vertices per warp and overflows to the next frontier), ``dense_threshold`` = fraction of
+    m above which a round runs bottom-up (symmetric graphs; the spec's 0 < t < 1, with 0 =
+    always and 1 = never allowed for the self-equivalence tests)."""
 
     tau: int = 512
     max_local_queue: int = 2048
@@ -107,30 +108,38 @@ class VgcConfig:
     def __post_init__(self):
         if not (1 <= self.tau <= self.max_local_queue):
             raise ValueError("need 1 <= tau <= max_local_queue")
-        if not 0 < self.dense_threshold < 1:
-            raise ValueError("need 0 < dense_threshold < 1")
+        if not 0 <= self.dense_threshold <= 1:
+            raise ValueError("need 0 <= dense_threshold <= 1")
 
 
-def bfs_parallel(g, source, cfg=None, device="cuda"):
+def bfs_parallel(g, source, cfg=None, device="cuda", symmetric=None, return_stats=False):
     """SPEC.md bfs_parallel: exact hop distances from ``source`` by the VGC frontier engine
-    (csrc/vgc.cu; pasgal_bfs_vgc): rounds of per-warp multi-hop local searches with
-    write-min distances.  Returns a DistanceArray whose ``rounds`` is the number of frontier
-    rounds (tau = 1: level-synchronous, eccentricity + 1 rounds)."""
+    (csrc/vgc.cu; pasgal_bfs_vgc_ex): rounds of per-warp multi-hop local searches with
+    write-min distances, and on a symmetric graph dense (bottom-up) rounds when the
+    frontier's out-degree sum exceeds ``cfg.dense_threshold * m`` (bfs_round_dense).
+    ``symmetric``: None checks it on the device (only when dense rounds can trigger).
+    Returns a DistanceArray whose ``rounds`` is the number of frontier rounds (tau = 1 and no
+    dense rounds: level-synchronous, eccentricity + 1 rounds); with ``return_stats`` also
+    ``{"dense_rounds": k}``."""
     cfg = cfg or VgcConfig()
     off, tgt = _device_csr(g, device)
     n = off.shape[0] - 1
     if not 0 <= source < n:
         raise ValueError(f"source {source} out of range for n={n}")
+    if symmetric is None:
+        symmetric = cfg.dense_threshold < 1 and _is_symmetric(off, tgt)
     lib = _lib.load()
     dist = torch.empty(n, dtype=torch.int32, device=off.device)
     ws = torch.empty(int(lib.pasgal_bfs_vgc_workspace_bytes(n)), dtype=torch.uint8, device=off.device)
     csr = _lib.PasgalCsr(n, tgt.shape[0], off.data_ptr(), tgt.data_ptr() if tgt.shape[0] else 0)
-    rounds = ctypes.c_int64()
-    st = lib.pasgal_bfs_vgc(ctypes.byref(csr), int(source), int(cfg.tau), ctypes.c_void_p(dist.data_ptr()),
-                            ctypes.byref(rounds), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                            ctypes.c_void_p(torch.cuda.current_stream(off.device).cuda_stream))
+    rounds, dense = ctypes.c_int64(), ctypes.c_int64()
+    st = lib.pasgal_bfs_vgc_ex(ctypes.byref(csr), int(source), int(cfg.tau), float(cfg.dense_threshold),
+                               int(bool(symmetric)), ctypes.c_void_p(dist.data_ptr()), ctypes.byref(rounds),
+                               ctypes.byref(dense), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                               ctypes.c_void_p(torch.cuda.current_stream(off.device).cuda_stream))
     _lib.check(st, "bfs_vgc")
-    return DistanceArray(dist.cpu().numpy().astype(np.int64), source, rounds=int(rounds.value))
+    res = DistanceArray(dist.cpu().numpy().astype(np.int64), source, rounds=int(rounds.value))
+    return (res, {"dense_rounds": int(dense.value)}) if return_stats else res
 
 
 def eccentricities(g, sources, device="cuda"):

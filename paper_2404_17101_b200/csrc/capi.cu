@@ -26,8 +26,8 @@ int bcc_graph_create(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* w
 int bcc_graph_launch(void* handle, cudaStream_t st, int* launches);
 void bcc_graph_destroy(void* handle);
 size_t vgc_bfs_workspace_bytes(int64_t n);
-int vgc_bfs(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* ws, size_t ws_bytes,
-            cudaStream_t st);
+int vgc_bfs(const pasgal_csr_t* g, int64_t source, int tau, double dense_threshold, int symmetric, int32_t* dist,
+            int64_t* rounds, int64_t* dense_rounds, void* ws, size_t ws_bytes, cudaStream_t st);
 int canonical_checksum(const uint32_t* lab, int64_t m, const uint32_t* bits, int64_t n, unsigned long long* out,
                        cudaStream_t st);
 int cc_launch(const pasgal_csr_t* g, uint32_t* comp, int64_t* count_dev, void* ws, size_t ws_bytes, u64 seed,
@@ -264,13 +264,20 @@ int pasgal_adj_parse(const uint8_t* text, int64_t nbytes, void* temp, size_t tem
 
 size_t pasgal_bfs_vgc_workspace_bytes(int64_t n) { return pg::vgc_bfs_workspace_bytes(n < 0 ? 0 : n); }
 
-int pasgal_bfs_vgc(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+int pasgal_bfs_vgc_ex(const pasgal_csr_t* g, int64_t source, int tau, double dense_threshold, int symmetric,
+                      int32_t* dist, int64_t* rounds, int64_t* dense_rounds, void* workspace, size_t workspace_bytes,
+                      void* stream) {
     int s = check_csr(g);
     if (s) return s;
-    if (source < 0 || source >= g->n || tau < 1 || !dist || !rounds) return PASGAL_EINVAL;
+    if (source < 0 || source >= g->n || tau < 1 || !dist || !rounds || !(dense_threshold >= 0.0)) return PASGAL_EINVAL;
     if (!workspace) return PASGAL_EWORKSPACE;
-    return pg::vgc_bfs(g, source, tau, dist, rounds, workspace, workspace_bytes, (cudaStream_t)stream);
+    return pg::vgc_bfs(g, source, tau, dense_threshold, symmetric, dist, rounds, dense_rounds, workspace,
+                       workspace_bytes, (cudaStream_t)stream);
+}
+
+int pasgal_bfs_vgc(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+    return pasgal_bfs_vgc_ex(g, source, tau, 1.0, 0, dist, rounds, nullptr, workspace, workspace_bytes, stream);
 }
 
 int pasgal_canonical_checksum(const uint32_t* labels, int64_t m_slots, const uint32_t* artic_bits, int64_t n,

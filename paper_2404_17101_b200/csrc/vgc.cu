@@ -16,6 +16,12 @@
 // whatever tau and the schedule.  tau = 1 is level-synchronous BFS (rounds = eccentricity
 // + 1); a larger tau needs fewer rounds.
 //
+// Dense rounds (SPEC.md bfs_round_dense, direction optimisation): on a symmetric graph, when
+// the frontier's out-degree sum exceeds dense_threshold * m, the round instead has every
+// vertex scan its own row for frontier members (a frontier bitmap, L2-resident) and take the
+// least d(u) + 1 among them -- the same relaxations as the top-down round, read as in-edges,
+// without atomics; improved vertices form the next frontier.
+//
 // Deviation from the SPEC's design ledger: the 16 overshoot buckets are replaced by the
 // per-round admission stamp (the spec's Open Questions allow any consistent reading; the
 // exactness and tau-invariance properties are what it requires, tests/test_vgc.py).
@@ -31,7 +37,8 @@ constexpr u32 VB_INF = 0x7FFFFFFFu;
 
 struct VgcWs {
     u32 *F[2], *STAMP;
-    u32* cnt;      // [0..1] frontier sizes, [2] take counter of the current round
+    u32* FB;       // frontier bitmap (dense rounds)
+    u32* cnt;      // [0..1] frontier sizes, [2] take counter of the current round, [4..5] u64 degree sum
 };
 
 static size_t vgc_carve(VgcWs& w, char* base, i64 n) {
@@ -46,6 +53,7 @@ static size_t vgc_carve(VgcWs& w, char* base, i64 n) {
     w.F[0] = (u32*)take(4 * nn);
     w.F[1] = (u32*)take(4 * nn);
     w.STAMP = (u32*)take(4 * nn);
+    w.FB = (u32*)take(4 * cdiv(nn, 32));
     w.cnt = (u32*)take(64);
     return o + 256;
 }
@@ -170,6 +178,52 @@ __global__ void __launch_bounds__(VB_WARPS * 32, 8) k_vb_round(const i64* __rest
     }
 }
 
+// out-degree sum of the frontier (the dense-round test), into the u64 at cnt + 4
+__global__ void k_vb_fdeg(const i64* __restrict__ off, const u32* __restrict__ FC, const u32* cnt, int cur,
+                          unsigned long long* dsum) {
+    const u32 nfc = cnt[cur];
+    u64 d = 0;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nfc; i += gridDim.x * blockDim.x) {
+        const u32 u = FC[i];
+        d += (u64)(off[(i64)u + 1] - off[u]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
+    if ((threadIdx.x & 31) == 0 && d) atomicAdd(dsum, (unsigned long long)d);
+}
+
+__global__ void k_vb_frontbits(const u32* __restrict__ FC, const u32* cnt, int cur, u32* FB) {
+    const u32 nfc = cnt[cur];
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nfc; i += gridDim.x * blockDim.x) {
+        const u32 u = FC[i];
+        atomicOr(FB + (u >> 5), 1u << (u & 31));
+    }
+}
+
+// dense (bottom-up) round: every vertex takes the least d(u) + 1 over its frontier neighbours
+__global__ void k_vb_dense(i64 n, const i64* __restrict__ off, const int32_t* __restrict__ tgt, int32_t* dist,
+                           const u32* __restrict__ FB, u32* FN, u32* cnt, int cur, u32* STAMP, u32 round) {
+    const int lane = threadIdx.x & 31;
+    u32* nfn = cnt + (cur ^ 1);
+    for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += (i64)gridDim.x * blockDim.x) {
+        const i64 v = base + threadIdx.x;
+        bool imp = false;
+        if (v < n) {
+            u32 best = VB_INF;
+            const i64 a = off[v], b = off[v + 1];
+            for (i64 sl = a; sl < b; ++sl) {
+                const u32 u = (u32)tgt[sl];
+                if ((__ldg(FB + (u >> 5)) >> (u & 31)) & 1u) {
+                    const u32 du = (u32)__ldcg(dist + u) + 1u;
+                    best = du < best ? du : best;
+                }
+            }
+            if (best < (u32)__ldcg(dist + v)) imp = (u32)atomicMin(dist + v, (int32_t)best) > best;
+        }
+        vb_admit(FN, nfn, STAMP, round, imp, (u32)v, lane);
+    }
+}
+
 __global__ void k_vb_next(u32* cnt, int cur) {
     cnt[cur] = 0;     // the frontier just consumed becomes the next round's output
     cnt[2] = 0;
@@ -199,8 +253,8 @@ static int vgc_grid_blocks() {
     return blocks;
 }
 
-int vgc_bfs(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64_t* rounds, void* ws_ptr,
-            size_t ws_bytes, cudaStream_t st) {
+int vgc_bfs(const pasgal_csr_t* g, int64_t source, int tau, double dense_threshold, int symmetric, int32_t* dist,
+            int64_t* rounds, int64_t* dense_rounds, void* ws_ptr, size_t ws_bytes, cudaStream_t st) {
     const i64 n = g->n;
     VgcWs w;
     if (ws_bytes < vgc_carve(w, nullptr, n)) return PASGAL_EWORKSPACE;
@@ -211,19 +265,41 @@ int vgc_bfs(const pasgal_csr_t* g, int64_t source, int tau, int32_t* dist, int64
     k_vb_source<<<1, 1, 0, st>>>((u32)source, dist, w.F[0], w.cnt);
     PG_LAUNCH_CHECK();
     const int grid = vgc_grid_blocks();
-    u32 host_cnt[2] = {1, 0};
-    int64_t r = 0;
+    const bool dense_ok = symmetric && dense_threshold < 1.0 && g->m_slots > 0;
+    unsigned long long* dsum = reinterpret_cast<unsigned long long*>(w.cnt + 4);
+    u32 host_cnt[6] = {1, 0, 0, 0, 0, 0};
+    int64_t r = 0, rd = 0;
     int cur = 0;
+    if (dense_ok) {
+        PG_CUDA_TRY(cudaMemsetAsync(dsum, 0, 8, st));
+        k_vb_fdeg<<<1, 256, 0, st>>>(g->offsets, w.F[0], w.cnt, 0, dsum);
+        PG_CUDA_TRY(cudaMemcpyAsync(host_cnt, w.cnt, 6 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        PG_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     while (host_cnt[cur] > 0) {
         ++r;
-        k_vb_round<<<grid, VB_WARPS * 32, 0, st>>>(g->offsets, g->targets, dist, w.F[cur], w.F[cur ^ 1], w.cnt, cur,
-                                                   w.STAMP, (u32)r, tau);
+        const u64 fdeg = (u64)host_cnt[4] | ((u64)host_cnt[5] << 32);
+        if (dense_ok && (double)fdeg > dense_threshold * (double)g->m_slots) {
+            ++rd;
+            PG_CUDA_TRY(cudaMemsetAsync(w.FB, 0, 4 * (size_t)cdiv(n, 32), st));
+            k_vb_frontbits<<<grid, 256, 0, st>>>(w.F[cur], w.cnt, cur, w.FB);
+            k_vb_dense<<<grid, 256, 0, st>>>(n, g->offsets, g->targets, dist, w.FB, w.F[cur ^ 1], w.cnt, cur,
+                                             w.STAMP, (u32)r);
+        } else {
+            k_vb_round<<<grid, VB_WARPS * 32, 0, st>>>(g->offsets, g->targets, dist, w.F[cur], w.F[cur ^ 1], w.cnt,
+                                                       cur, w.STAMP, (u32)r, tau);
+        }
         k_vb_next<<<1, 1, 0, st>>>(w.cnt, cur);
         PG_LAUNCH_CHECK();
         cur ^= 1;
-        PG_CUDA_TRY(cudaMemcpyAsync(host_cnt, w.cnt, 2 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        if (dense_ok) {
+            PG_CUDA_TRY(cudaMemsetAsync(dsum, 0, 8, st));
+            k_vb_fdeg<<<grid, 256, 0, st>>>(g->offsets, w.F[cur], w.cnt, cur, dsum);
+        }
+        PG_CUDA_TRY(cudaMemcpyAsync(host_cnt, w.cnt, 6 * sizeof(u32), cudaMemcpyDeviceToHost, st));
         PG_CUDA_TRY(cudaStreamSynchronize(st));
     }
+    if (dense_rounds) *dense_rounds = rd;
     k_vb_finish<<<nb, B, 0, st>>>(n, dist);
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(cudaStreamSynchronize(st));

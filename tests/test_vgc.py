@@ -28,6 +28,7 @@ def test_vgc_config_validation():
         pg.VgcConfig(tau=10, max_local_queue=5)
     with pytest.raises(ValueError):
         pg.VgcConfig(dense_threshold=1.5)
+    assert pg.VgcConfig(dense_threshold=0.0).dense_threshold == 0.0       # always dense (tests)
 
 
 def _golden_cases():
@@ -138,3 +139,63 @@ def test_vgc_bfs_large_diameter_grid_against_device_queue_bfs():
     assert np.array_equal(r1.dist, want) and np.array_equal(rk.dist, want)
     assert r1.rounds == int(want.max()) + 1
     assert rk.rounds * 4 <= r1.rounds, (r1.rounds, rk.rounds)
+
+
+def _sym_random(rng, n, m):
+    src = rng.integers(0, n, size=m)
+    dst = rng.integers(0, n, size=m)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    s2, d2 = np.concatenate([src, dst]), np.concatenate([dst, src])
+    key = np.unique(s2 * n + d2)
+    s2, d2 = key // n, key % n
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(s2, minlength=n), out=off[1:])
+    return off, d2.astype(np.uint32)
+
+
+@pytest.mark.gpu
+def test_vgc_dense_rounds_equal_top_down():
+    """SPEC bfs_round_dense: forced dense_threshold=0 (every round bottom-up) vs 1 (never)
+    give identical DistanceArrays on 100 random symmetric graphs, for several tau; both
+    equal the queue-BFS oracle."""
+    import paper_2404_17101_b200 as pg
+
+    rng = np.random.default_rng(2025)
+    for i in range(100):
+        n = int(rng.integers(2, 1500))
+        off, tgt = _sym_random(rng, n, int(rng.integers(0, 6 * n)))
+        s = int(rng.integers(0, n))
+        tau = TAUS[i % len(TAUS)]
+        g = _G(off, tgt)
+        d0, st0 = pg.bfs_parallel(g, s, pg.VgcConfig(tau=tau, max_local_queue=max(tau, 2048), dense_threshold=0.0),
+                                  symmetric=True, return_stats=True)
+        d1, st1 = pg.bfs_parallel(g, s, pg.VgcConfig(tau=tau, max_local_queue=max(tau, 2048), dense_threshold=1.0),
+                                  symmetric=True, return_stats=True)
+        want, _ = oracle.bfs_queue(off, tgt, s)
+        assert np.array_equal(d0.dist, d1.dist) and np.array_equal(d0.dist, want), (i, tau)
+        assert st1["dense_rounds"] == 0
+        if off[s + 1] > off[s]:                                  # threshold 0: rounds with edges go dense
+            assert st0["dense_rounds"] >= 1
+    # complete graph K_8 from any source: one dense round reaches everything at distance 1
+    n = 8
+    src = np.repeat(np.arange(n), n - 1)
+    dst = np.array([w for u in range(n) for w in range(n) if w != u])
+    off = np.arange(0, n * (n - 1) + 1, n - 1, dtype=np.int64)
+    for s in range(n):
+        d, st = pg.bfs_parallel(_G(off, dst), s, pg.VgcConfig(tau=1), symmetric=None, return_stats=True)
+        assert st["dense_rounds"] >= 1 and d.dist[s] == 0 and (np.delete(d.dist, s) == 1).all()
+    del src
+
+
+@pytest.mark.gpu
+def test_vgc_dense_rounds_on_rmat():
+    """A low-diameter power-law graph (C2): with the default threshold the middle rounds go
+    bottom-up; distances equal the bit-parallel BFS."""
+    import paper_2404_17101_b200 as pg
+
+    dg = pg.make_config("c2")
+    want = pg.bfs(dg, 0).dist
+    d, st = pg.bfs_parallel(dg, 0, pg.VgcConfig(tau=1), return_stats=True)
+    assert np.array_equal(d.dist, want)
+    assert st["dense_rounds"] >= 1
