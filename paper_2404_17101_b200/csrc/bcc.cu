@@ -884,19 +884,33 @@ __global__ void k_forest_marks(i64 n, const uint2* __restrict__ HAB, ForestMarks
     const unsigned rb = __ballot_sync(0xFFFFFFFFu, x < n && !hooked);
     if (lane == 0 && x < n) fm.ROOT[x >> 5] = rb;
     const unsigned act = __ballot_sync(0xFFFFFFFFu, hooked);
+    if (!hooked) return;
+    // both endpoints' words read together (one L2 round trip), then at most one returning
+    // atomic per endpoint group
+    u32 v[2], t[2], o[2];
+    bool lead[2], many[2];
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
-        if (!hooked) continue;
-        const u32 v = d ? e.y : e.x;
-        const unsigned grp = __match_any_sync(act, v);
-        if (lane != __ffs(grp) - 1) continue;
-        // read first: a hub's bits are set after its first sightings, and the atomics of
-        // every later warp on one word would serialise at its L2 slice (10 ms at C5a)
-        const u32 bit = 1u << (v & 31);
-        if (__ldcg(fm.TWO + (v >> 5)) & bit) continue;
-        const bool many = __popc(grp) > 1;
-        const u32 old = (!many && (__ldcg(fm.ONE + (v >> 5)) & bit)) ? bit : atomicOr(fm.ONE + (v >> 5), bit);
-        if ((old & bit) || many) atomicOr(fm.TWO + (v >> 5), bit);
+        v[d] = d ? e.y : e.x;
+        const unsigned grp = __match_any_sync(act, v[d]);
+        lead[d] = lane == __ffs(grp) - 1;
+        many[d] = __popc(grp) > 1;
+    }
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+        t[d] = lead[d] ? __ldcg(fm.TWO + (v[d] >> 5)) : 0u;
+        o[d] = lead[d] ? __ldcg(fm.ONE + (v[d] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+        const u32 bit = 1u << (v[d] & 31);
+        if (!lead[d] || (t[d] & bit)) continue;     // a hub's bits are set after its first sightings
+        bool second = many[d] || (o[d] & bit);
+        if (!(o[d] & bit)) {                         // ONE must hold for every endpoint (isolated test)
+            const u32 old = atomicOr(fm.ONE + (v[d] >> 5), bit);
+            second = second || (old & bit);
+        }
+        if (second) atomicOr(fm.TWO + (v[d] >> 5), bit);
     }
 }
 
