@@ -782,7 +782,10 @@ __device__ __forceinline__ void arc_splice(u32* NEXT, const ArcGroup& g, u32 arc
 // hubs: per-warp aggregation still left ~5M returning exchanges on the top hub's HEAD,
 // serialised at one L2 slice; per-block aggregation divides that by the block size and
 // keeps each hub's list in runs of consecutive hooked ids.
-constexpr int AL_T = 512, AL_H = 2048;     // <= 2 keys per thread: the table stays half empty
+#ifndef PG_AL_LOG
+#define PG_AL_LOG 9
+#endif
+constexpr int AL_T = 1 << PG_AL_LOG, AL_H = 4 * AL_T;   // <= 2 keys per thread: the table stays half empty
 // Leaf trimming: a non-root vertex of forest degree 1 is a leaf of the rooted forest
 // whatever the rooting (C5a: most forest vertices are leaves hooked onto hubs), so its edge
 // is kept off the Euler tour.  The edge's record gets a tag naming the leaf end and the
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(AL_T) k_arc_link_blk(i64 n, uint2* HAB, u32* H
     const i64 x = (i64)blockIdx.x * AL_T + threadIdx.x;
     const uint2 e = x < n ? HAB[2 * x] : make_uint2(PG_INV, PG_INV);
     auto slot_of = [&](u32 key) -> u32 {
-        u32 h = (key * 0x9E3779B1u) >> (32 - 11);           // AL_H = 2^11 slots
+        u32 h = (key * 0x9E3779B1u) >> (32 - (PG_AL_LOG + 2));   // AL_H slots
         for (;;) {
             const u32 k = atomicCAS(hkey + h, PG_INV, key);
             if (k == PG_INV || k == key) return h;
@@ -2082,7 +2085,7 @@ static int vgc_tau() {
 // lattice (C3: +0.5 ms).  PASGAL_BCC_TRIM=0/1 forces it (A/B sweeps).  Tour positions must
 // stay below the HAB tags (n < 2^31 - 2).
 static bool leaf_trim(i64 n, i64 m) {
-    static const char* e = getenv("PASGAL_BCC_TRIM");
+    const char* e = getenv("PASGAL_BCC_TRIM");
     if (n < 64 || n >= ((i64)1 << 31) - 2) return false;
     if (e) return e[0] != '0';
     return m >= 4 * n;

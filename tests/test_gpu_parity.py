@@ -524,3 +524,89 @@ def test_config_full_size_against_python_reference_hashes(name):
         assert int(art.sum()) == want["artic_count"]
         assert h(art) == want["artic"], (name, seed)
         assert h(lab) == want["labels"], (name, seed)
+
+
+def _star_forest_cases():
+    """Shapes whose spanning forests are leafy: stars (a root whose children are all leaves:
+    the empty-list root of leaf trimming), double stars, caterpillars, random trees and a
+    star with parallel edges and a self-loop."""
+    rng = np.random.default_rng(77)
+
+    def csr(n, edges):
+        e = np.array(edges, dtype=np.int64).reshape(-1, 2)
+        s = np.concatenate([e[:, 0], e[:, 1]])
+        d = np.concatenate([e[:, 1], e[:, 0]])
+        o = np.lexsort((d, s))
+        off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(s[o], minlength=n), out=off[1:])
+        return off, d[o].astype(np.uint32)
+
+    n = 5000
+    yield "star", *csr(n, [(0, i) for i in range(1, n)])
+    yield "star_mid_centre", *csr(n, [(n // 2, i) for i in range(n) if i != n // 2])
+    yield "double_star", *csr(n, [(0, 1)] + [(i % 2, i) for i in range(2, n)])
+    yield "caterpillar", *csr(n, [(i, i + 1) for i in range(0, 100)] + [(i % 100, i) for i in range(101, n)])
+    par = rng.integers(0, np.arange(1, n))
+    yield "random_tree", *csr(n, list(zip(par.tolist(), range(1, n))))
+    e = [(0, i) for i in range(1, 300)] + [(0, 5), (0, 7), (3, 3), (10, 11)]
+    yield "star_multi_selfloop", *csr(300, e)
+    yield "two_stars_and_isolated", *csr(400, [(0, i) for i in range(1, 150)] + [(200, i) for i in range(201, 350)])
+
+
+@pytest.mark.parametrize("trim", ["1", "0"])
+def test_leaf_trimming_on_leafy_forests(trim, monkeypatch):
+    """Leaf trimming forced on and off (PASGAL_BCC_TRIM) on leafy forests and on the corpus:
+    canonical labels, articulation and count equal to the C oracle either way."""
+    monkeypatch.setenv("PASGAL_BCC_TRIM", trim)
+    for name, off, tgt in _star_forest_cases():
+        ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+        want = oracle.canonical_min_eid(off, tgt, ref.edge_label)
+        d_off = torch.from_numpy(off).cuda()
+        d_tgt = torch.from_numpy(tgt.view(np.int32)).cuda()
+        lab, art, cnt = _host_out(pg.bcc_device(d_off, d_tgt, canonical=True), off.shape[0] - 1)
+        assert cnt == ref.bcc_count, name
+        assert np.array_equal(art, ref.articulation.astype(bool)), name
+        assert np.array_equal(lab, want), name
+        # vertex mode: the O(n) result gives the same partition by the reference's rule
+        res = pg.bcc(pg.Graph(off, tgt), edge_labels=False)
+        assert res.bcc_count == ref.bcc_count, name
+        keep = np.repeat(np.arange(off.shape[0] - 1), np.diff(off)) < tgt.astype(np.int64)
+        got = pg.canonical_relabel(res.edge_labels(pg.Graph(off, tgt))[keep])
+        assert np.array_equal(got, pg.canonical_relabel(want[keep].astype(np.int64))), name
+    for case in list(golden_io.corpus())[:60]:
+        check_case(case)
+
+
+def test_degenerate_graphs_all_modes():
+    """n = 0, n = 1, only isolated vertices, a single edge: per-slot, canonical, vertex mode
+    and CUDA-graph replay all return the oracle's answer."""
+    for n, edges in [(0, []), (1, []), (70, []), (2, [(0, 1)]), (80, [(5, 6)])]:
+        s = np.array([u for u, v in edges] + [v for u, v in edges], dtype=np.int64)
+        d = np.array([v for u, v in edges] + [u for u, v in edges], dtype=np.int64)
+        o = np.lexsort((d, s))
+        off = np.zeros(n + 1, dtype=np.int64)
+        if n:
+            np.cumsum(np.bincount(s[o], minlength=n), out=off[1:])
+        tgt = d[o].astype(np.uint32)
+        g = pg.Graph(off, tgt)
+        r = pg.bcc(g)
+        r2 = pg.bcc(g, edge_labels=False)
+        if n:
+            ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+            assert r.bcc_count == r2.bcc_count == ref.bcc_count
+            assert np.array_equal(r.articulation, ref.articulation.astype(bool))
+            assert np.array_equal(r2.articulation, ref.articulation.astype(bool))
+        else:
+            assert r.bcc_count == r2.bcc_count == 0
+        if n:
+            d_off = torch.from_numpy(off).cuda()
+            d_tgt = torch.from_numpy(tgt.view(np.int32)).cuda()
+            m = tgt.shape[0]
+            ws = torch.empty(pg.workspace_bytes(n, m), dtype=torch.uint8, device="cuda")
+            out = pg.DeviceBcc(edge_label=torch.empty(max(m, 1), dtype=torch.int32, device="cuda"),
+                               artic_bits=torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda"),
+                               bcc_count=torch.empty(1, dtype=torch.int64, device="cuda"))
+            for _ in range(2):
+                rr = pg.bcc_device(d_off, d_tgt, out=out, workspace=ws, graph=True)
+                assert int(rr.bcc_count.item()) == ref.bcc_count
+    pg.release_workspace()
