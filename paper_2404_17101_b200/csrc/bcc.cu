@@ -923,7 +923,6 @@ __global__ void k_forest_marks(i64 n, const uint2* __restrict__ HAB, ForestMarks
 //   otherwise succ(2r) = NEXT[2r+1] = first out-arc of r, and succ(2r+1) = NEXT[2r] = the
 //   down arc of the root chained before r (warp-aggregated atomicExch on ctr->roothead).
 // Neither the order of trees on the tour nor the order of isolated slots matters.
-constexpr u64 M31 = (1ull << 31) - 1;
 
 struct IsoOut {
     uint2* FL;
