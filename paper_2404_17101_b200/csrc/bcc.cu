@@ -34,8 +34,8 @@
 namespace pg {
 
 constexpr u32 VFLAG = 0x80000000u;     // tour payload: arc is a root's virtual down arc
-// HAB[2x+1].x tags.  Tour arcs hold positions there, which stay below TAG_ISO (n < 2^31 - 2).
-constexpr u32 TAG_ISO = 0xFFFFFFFCu;    // x is an isolated vertex (no forest edge)
+// HAB[2x+1].x tags of trimmed edges.  Tour arcs hold positions there, which stay below the
+// tags (n < 2^31 - 2).
 constexpr u32 TAG_TRIM_A = 0xFFFFFFFEu; // edge x trimmed: its endpoint .x is a forest leaf
 constexpr u32 TAG_TRIM_B = 0xFFFFFFFDu; // edge x trimmed: its endpoint .y is a forest leaf
 #ifndef PG_LABELS_MINB
@@ -958,7 +958,6 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, uint2* HAB, const u32
         const bool iso = root && (fm.ONE ? !fm_bit(fm.ONE, (u32)x) : h == PG_INV);
         const bool chain = root && !iso;
         const bool trimmed = rec.z == TAG_TRIM_A || rec.z == TAG_TRIM_B;
-        if (iso) reinterpret_cast<uint4*>(HAB)[x] = make_uint4(rec.x, rec.y, TAG_ISO, rec.w);
         if (x < n && !root && !trimmed) {
 #pragma unroll
             for (int d = 0; d < 2; ++d) {
@@ -1033,27 +1032,31 @@ __device__ __forceinline__ TourInfo tour_info(const Ctr* ctr, i64 n) {
     t.len = (u32)(2 * (n - (i64)ctr->niso - (i64)ctr->ntrim));
     return t;
 }
+// a ruler is an on-tour arc: not an arc of a trimmed leaf edge (record tag) nor of an
+// isolated vertex (a root without forest edges: ONE map with trimming, empty list without)
 __device__ __forceinline__ bool ruler_start(i64 s, i64 nsk, const TourInfo& t, const uint2* HAB, const u32* HEAD,
-                                            u32 lrs, u32& x) {
+                                            const u32* ONE, u32 lrs, u32& x) {
     if (s < nsk) {
         x = (u32)s << lrs;
-        u32 v = x >> 1;
-        (void)HEAD;
-        return HAB[2 * (i64)v + 1].x < TAG_ISO;   // isolated vertices and trimmed leaves' edges are off the tour
+        const u32 v = x >> 1;
+        const uint4 rec = reinterpret_cast<const uint4*>(HAB)[v];
+        if (rec.z == TAG_TRIM_A || rec.z == TAG_TRIM_B) return false;
+        if (rec.x != PG_INV) return true;
+        return ONE ? ((ONE[v >> 5] >> (v & 31)) & 1u) != 0 : HEAD[v] != PG_INV;
     }
     x = t.head;
     return t.head != PG_INV && (t.head & ((1u << lrs) - 1u)) != 0;
 }
 
 __global__ void k_lr_walk1(i64 n, i64 ns, u32 lrs, const u32* __restrict__ NEXT, const uint2* __restrict__ HAB,
-                           const u32* __restrict__ HEAD, const Ctr* ctr, u32* SPLEN,
+                           const u32* __restrict__ HEAD, const u32* __restrict__ ONE, const Ctr* ctr, u32* SPLEN,
                            u32* SPNEXT) {
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const TourInfo t = tour_info(ctr, n);
     const i64 nsk = ns - 1;
     u32 x;
-    if (!ruler_start(s, nsk, t, HAB, HEAD, lrs, x)) {
+    if (!ruler_start(s, nsk, t, HAB, HEAD, ONE, lrs, x)) {
         SPLEN[s] = 0;
         SPNEXT[s] = PG_INV;
         return;
@@ -1129,14 +1132,14 @@ constexpr int LR_T = 256;
 
 __global__ void __launch_bounds__(LR_T) k_lr_walk2(i64 n, i64 ns, u32 lrs, const u32* __restrict__ NEXT,
                                                    const uint2* __restrict__ HAB, const u32* __restrict__ HEAD,
-                                                   const Ctr* ctr, const u32* __restrict__ SUFFIX, uint2* HABW,
-                                                   u32* TA) {
+                                                   const u32* __restrict__ ONE, const Ctr* ctr,
+                                                   const u32* __restrict__ SUFFIX, uint2* HABW, u32* TA) {
     __shared__ __align__(16) u32 lr_buf[LR_T * 8];
     i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const TourInfo t = tour_info(ctr, n);
     u32 x;
-    if (!ruler_start(s, ns - 1, t, HAB, HEAD, lrs, x)) return;
+    if (!ruler_start(s, ns - 1, t, HAB, HEAD, ONE, lrs, x)) return;
     const u32 pos0 = t.len - SUFFIX[s];
     u32 pos = pos0;
     // TA[pos] = arc, staged per thread so that whole 32-byte sectors (8 positions, aligned)
@@ -2244,8 +2247,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
-    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[0],
-                                                     w.SPNEXT[0]));
+    PG_K(k_lr_walk1<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, fm.ONE, w.ctr,
+                                                     w.SPLEN[0], w.SPNEXT[0]));
     int cur = 0;
     if (w.ns <= WY_MAX) {
         const size_t smem = 2 * sizeof(u32) * WY_MAX;
@@ -2258,8 +2261,8 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
             cur ^= 1;
         }
     }
-    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, w.ctr, w.SPLEN[cur],
-                                                     w.HAB, w.TA));
+    PG_K(k_lr_walk2<<<nblk(w.ns, 128), 128, 0, st>>>(n, w.ns, w.lrs, w.NEXT, w.HAB, w.HEAD, fm.ONE, w.ctr,
+                                                     w.SPLEN[cur], w.HAB, w.TA));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LISTRANK));
     PG_CUDA_TRY(launch_scan<u32>(L, w.SCAN, 0u, SumOp(), PreLoad{w.TA, w.HAB, w.T, w.TP, w.ctr, n, LCNT},
