@@ -2081,16 +2081,16 @@ static int vgc_tau() {
     const char* t = getenv("PASGAL_BCC_VGC_TAU");
     return t && atoi(t) > 0 ? atoi(t) : VGC_TAU_DEFAULT;
 }
-// Leaf trimming of the Euler tour (S3) pays where the spanning forest is leafy: the sampled
-// union-find forest of a graph with >= 4 slots per vertex (RMAT, kNN: most vertices hook onto
-// a neighbour and nothing hooks onto them; C5a rooting 31.8 -> 28 ms, C4 -1.2 ms), not on a
-// lattice (C3: +0.5 ms).  PASGAL_BCC_TRIM=0/1 forces it (A/B sweeps).  Tour positions must
+// Leaf trimming of the Euler tour (S3) pays where the spanning forest is leafy and large: the
+// sampled union-find forest of a graph with >= 4 slots per vertex (RMAT, kNN: most vertices
+// hook onto a neighbour and nothing hooks onto them; C5a rooting 31.8 -> 27.5 ms, C4 -1.2 ms),
+// not on a lattice (C3: +0.8 ms) nor on small graphs.  PASGAL_BCC_TRIM=0/1 forces it (A/B sweeps).  Tour positions must
 // stay below the HAB tags (n < 2^31 - 2).
 static bool leaf_trim(i64 n, i64 m) {
     const char* e = getenv("PASGAL_BCC_TRIM");
     if (n < 64 || n >= ((i64)1 << 31) - 2) return false;
     if (e) return e[0] != '0';
-    return m >= 4 * n;
+    return m >= 4 * n && n >= ((i64)1 << 22);   // below 2^22 (C2: 1.21 -> 1.35 ms) the fixed costs win
 }
 
 static unsigned vgc_grid() {
