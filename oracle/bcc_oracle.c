@@ -83,21 +83,19 @@ static int twin_and_symmetry(int64_t n, const int64_t* off, const uint32_t* tgt,
     for (int64_t e = 0; e < m; ++e) rev[cnt[tgt[e]]++] = (uint32_t)e;
     /* symmetric iff sorted (src,dst) keys == sorted (dst,src) keys, position by position;
      * twin[fwd[k]] = rev[k] (the reference's pairing). */
+    /* src of every slot (n < 2^31), so the pairing below reads it with one access */
+    uint32_t* src = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m);
+    if (!src) { free(fwd); free(rev); free(cnt); *status = ORC_NOMEM; return 0; }
+    for (int64_t v = 0; v < n; ++v)
+        for (int64_t e = off[v]; e < off[v + 1]; ++e) src[e] = (uint32_t)v;
     int sym = 1;
-    int64_t u = 0, ru = 0;
     for (int64_t k = 0; k < m && sym; ++k) {
-        while (off[u + 1] <= k) ++u;          /* fwd[k] lies in row u (fwd permutes within rows) */
         int64_t ef = fwd ? fwd[k] : k, er = rev[k];
-        /* src of er: rev is ordered by dst, so walk its row pointer forward when possible */
-        if (off[ru] > er || off[ru + 1] <= er) {
-            int64_t lo = 0, hi = n - 1;
-            while (lo < hi) { int64_t mid = (lo + hi + 1) / 2; if (off[mid] <= er) lo = mid; else hi = mid - 1; }
-            ru = lo;
-        }
-        if ((uint64_t)u != tgt[er] || (uint64_t)tgt[ef] != (uint64_t)ru) sym = 0;
+        /* fwd permutes within rows, so src[ef] == src[k] */
+        if (src[k] != tgt[er] || tgt[ef] != src[er]) sym = 0;
         twin[ef] = (uint32_t)er;
     }
-    free(fwd); free(rev); free(cnt);
+    free(fwd); free(rev); free(cnt); free(src);
     return sym;
 }
 

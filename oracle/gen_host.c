@@ -149,7 +149,10 @@ int64_t host_knn_keys(int64_t npts, int k, const uint32_t* X, const uint32_t* Y,
     uint64_t bd[64]; uint32_t bj[64];
     int64_t nk = 0;
     int64_t cs = (int64_t)1 << sh;
-    for (int64_t i = 0; i < npts; ++i) {
+    /* points are visited in cell order (neighbouring cells stay cached); the key order
+     * does not matter, csr_from_keys sorts them */
+    for (int64_t oi = 0; oi < npts; ++oi) {
+        int64_t i = order[oi];
         int cnt = 0;
         int64_t cx = X[i] >> sh, cy = Y[i] >> sh;
         for (int64_t r = 0;; ++r) {
