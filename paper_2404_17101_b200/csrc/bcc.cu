@@ -1307,8 +1307,7 @@ __global__ void k_vertex_first(i64 n, uint2* FL, const u32* __restrict__ PPAR, u
 // --------------------------------------------------------------------------
 // S4: tags  w1/w2[first[v]] = min/max(first[v], first[u] for all neighbours u)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ void write_tag(uint2* W, const u32* FIRST, u32 row, u32 mn, u32 mx, bool atomic) {
-    u32 f = __ldg(FIRST + row);
+__device__ __forceinline__ void write_tag(uint2* W, u32 f, u32 mn, u32 mx, bool atomic) {
     if (atomic) {
         atomicMin(&W[f].x, mn);
         atomicMax(&W[f].y, mx);
@@ -1334,7 +1333,8 @@ template <bool NOL1>
 __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64* __restrict__ off,
                                                                 const int32_t* __restrict__ tgt, i64 n, i64 m,
                                                                 const u32* __restrict__ crow,
-                                                                const u32* __restrict__ FIRST, uint2* W) {
+                                                                const u32* __restrict__ FIRST, uint2* W,
+                                                                u32* __restrict__ DIR) {
     __shared__ BlkSmem smem[WCH_BLOCK / 32];
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
@@ -1358,24 +1358,31 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
         for (int k = 0; k < WCH_U; ++k)
             if (s0 + 32 * k + lane < s1) g[k] = NOL1 ? ld_keep(FIRST + g[k], pol) : ld_keep_l1(FIRST + g[k], pol);
         if (one_row) {   // warp-uniform
-            u32 mn = PG_INV, mx = 0;
+            const u32 fb = __ldg(FIRST + base);
+            u32 mn = PG_INV, mx = 0, dw = 0;
 #pragma unroll
-            for (int k = 0; k < WCH_U; ++k)
-                if (s0 + 32 * k + lane < s1) {
+            for (int k = 0; k < WCH_U; ++k) {
+                const bool ok = s0 + 32 * k + lane < s1;
+                if (ok) {
                     mn = g[k] < mn ? g[k] : mn;
                     mx = g[k] > mx ? g[k] : mx;
                 }
+                const unsigned b = __ballot_sync(0xFFFFFFFFu, ok && g[k] > fb);
+                if (lane == k) dw = b;
+            }
+            if (DIR && lane < WCH_U) DIR[(i64)WCH_U * c + lane] = dw;
             mn = __reduce_min_sync(0xFFFFFFFFu, mn);
             mx = __reduce_max_sync(0xFFFFFFFFu, mx);
-            if (lane == 0) write_tag(W, FIRST, base, mn, mx, a_base < s0 || e_base > s1);
+            if (lane == 0) write_tag(W, fb, mn, mx, a_base < s0 || e_base > s1);
             return;
         }
         blk_transpose(sm, lane, g, fw);
     }
     const BlkRows br = blk_rows(off, n, s0, s1, base, lane, sm);
     const bool hstart = br.mb & 1u;
-    u32 r = br.r_first;
-    u32 mn = PG_INV, mx = 0, hmn = PG_INV, hmx = 0;
+    const u32 fh = __ldg(FIRST + br.r_first);    // the head row's preorder position
+    u32 fr = fh;                                  // the current row's
+    u32 mn = PG_INV, mx = 0, hmn = PG_INV, hmx = 0, db = 0;
     bool in_head = true;
 #pragma unroll
     for (int i = 0; i < BLK_SPL; ++i) {
@@ -1384,18 +1391,25 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
                 hmn = mn;
                 hmx = mx;
                 in_head = false;
-                if (hstart) write_tag(W, FIRST, r, mn, mx, false);   // began at p0: complete
+                if (hstart) write_tag(W, fr, mn, mx, false);   // began at p0: complete
             } else {
-                write_tag(W, FIRST, r, mn, mx, false);               // began and ended in the lane
+                write_tag(W, fr, mn, mx, false);               // began and ended in the lane
             }
-            r = sm.row[BLK_SPL * lane + i];
+            fr = __ldg(FIRST + sm.row[BLK_SPL * lane + i]);
             mn = PG_INV;
             mx = 0;
         }
         if (sl + i < s1) {
             mn = fw[i] < mn ? fw[i] : mn;
             mx = fw[i] > mx ? fw[i] : mx;
+            db |= (u32)(fw[i] > fr) << i;
         }
+    }
+    if (DIR) {   // slot 8l+i -> bit 8(l&3)+i of word l>>2 (= slot order)
+        u32 x = db << (8 * (lane & 3));
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        if ((lane & 3) == 0) DIR[(i64)WCH_U * c + (lane >> 2)] = x;
     }
     // mn/mx: the lane's last row, open to the right; scan it across lanes
     const bool inner = (br.mb & 0xFEu) != 0;
@@ -1407,12 +1421,12 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
     if (inner && !hstart) {                      // head row came from the left and ends here
         const u32 tmn = lane > 0 && pmn < hmn ? pmn : hmn;
         const u32 tmx = lane > 0 && pmx > hmx ? pmx : hmx;
-        write_tag(W, FIRST, br.r_first, tmn, tmx, !pstarted);
+        write_tag(W, fh, tmn, tmx, !pstarted);
     }
     // the lane's last row ends exactly at the lane's end when the next lane starts a row
     const bool next_starts = __shfl_down_sync(0xFFFFFFFFu, (int)hstart, 1) != 0;
-    if (lane < 31 && next_starts) write_tag(W, FIRST, r, cmn, cmx, !started);
-    if (lane == 31) write_tag(W, FIRST, r, cmn, cmx, !started || br.last_open);
+    if (lane < 31 && next_starts) write_tag(W, fr, cmn, cmx, !started);
+    if (lane == 31) write_tag(W, fr, cmn, cmx, !started || br.last_open);
 }
 
 // --------------------------------------------------------------------------
@@ -1735,12 +1749,13 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
 // component, so the target's component comes from the L2-resident membership bitmap and
 // only the remaining slots gather CIDV from HBM.
 #ifndef PG_LABELS_HALVES
-#define PG_LABELS_HALVES 4
+#define PG_LABELS_HALVES 8
 #endif
 __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
                                                       const u32* __restrict__ CIDV, const u32* __restrict__ GBIT,
-                                                      const Ctr* __restrict__ ctr, u32* label) {
+                                                      const Ctr* __restrict__ ctr, const u32* __restrict__ DIR,
+                                                      u32* label) {
     const int lane = threadIdx.x & 31;
     const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
     if (c >= num_chunks(m)) return;
@@ -1752,6 +1767,11 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
         i64 s = s0 + 32 * k + lane;
         w[k] = s < s1 ? (u32)__ldcs(tgt + s) : 0u;
     }
+    // direction bits from k_tags_blk: a slot whose target lies earlier in preorder takes its
+    // row's component (the row is the deeper endpoint), so only the other half looks up
+    // the target (without DIR every slot does)
+    u32 dmask = 0xFFFFFFFFu;
+    if (DIR) dmask = __ldcs(DIR + (i64)WCH_U * c + (lane & (WCH_U - 1)));
     // the chunk in PG_LABELS_HALVES parts: fewer live registers (32 per thread, no spills)
     constexpr int H = WCH_U / PG_LABELS_HALVES;
     u32 cur = crow[c];
@@ -1768,15 +1788,17 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
                 cur = __shfl_sync(0xFFFFFFFFu, rw[k], 31);
             }
         }
+        u32 look = 0;
 #pragma unroll
         for (int k = 0; k < H; ++k) {
             i64 s = s0 + 32 * (h + k) + lane;
-            cw[k] = s < s1 ? __ldg(GBIT + (w[h + k] >> 5)) : 0u;
+            const bool lk = s < s1 && ((__shfl_sync(0xFFFFFFFFu, dmask, h + k) >> lane) & 1u);
+            look |= (u32)lk << k;
+            cw[k] = lk ? __ldg(GBIT + (w[h + k] >> 5)) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            i64 s = s0 + 32 * (h + k) + lane;
-            cw[k] = (cw[k] >> (w[h + k] & 31)) & 1u ? g : (s < s1 ? ld_na(CIDV + w[h + k]) : 0u);
+            cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : ld_na(CIDV + w[h + k]);
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
@@ -2093,6 +2115,13 @@ static bool leaf_trim(i64 n, i64 m) {
     return m >= 4 * n && n >= ((i64)1 << 22);   // below 2^22 (C2: 1.21 -> 1.35 ms) the fixed costs win
 }
 
+// The direction bits (M/8 bytes) live in the dead Euler-tour array T (16 bytes per vertex).
+static bool dir_bits(i64 n, i64 m) {
+    const char* e = getenv("PASGAL_BCC_DIR");
+    if (e && e[0] == '0') return false;
+    return (u64)cdiv(m, WCH) * WCH / 8 <= (u64)16 * (u64)(n > 0 ? n : 1);
+}
+
 static unsigned vgc_grid() {
     static int blocks = 0;
     if (!blocks) {
@@ -2279,11 +2308,14 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
+    // per-slot direction bits for the labels pass (first[target] > first[row]), M/8 bytes in
+    // the Euler-tour array T (dead after the tour stage; room for up to 128 slots per vertex)
+    u32* dir = out->edge_label && dir_bits(n, m) ? (u32*)w.T : nullptr;
     if (w.nch > 0) {
         if (n >= ((i64)1 << 22))
-            PG_K(k_tags_blk<true><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+            PG_K(k_tags_blk<true><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W, dir));
         else
-            PG_K(k_tags_blk<false><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W));
+            PG_K(k_tags_blk<false><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W, dir));
     }
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
@@ -2313,8 +2345,9 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
-    if (w.nch > 0 && out->edge_label) PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, w.GBIT, w.ctr,
-                                                                          out->edge_label));
+    if (w.nch > 0 && out->edge_label)
+        PG_K(k_labels<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.CIDV, w.GBIT, w.ctr, dir,
+                                                             out->edge_label));
     PG_K(k_finish<<<1, 1, 0, st>>>(w.ctr, out->bcc_count));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LABELS));
