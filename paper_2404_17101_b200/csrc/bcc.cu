@@ -1430,6 +1430,301 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS_MINB) k_tags_blk(const i64*
 }
 
 // --------------------------------------------------------------------------
+// S4, two-level tags (large graphs).  A per-slot gather of FIRST (4 B per vertex: 1 GB at
+// 2^28 vertices, 8x the L2) misses L2 on most slots and moves a 32-byte sector for 4 useful
+// bytes (k_tags_blk at C5a: 137 GB of DRAM for 39 GB algorithmic).  But a row only needs its
+// min and max.  So every vertex also gets a CODE of TAG_BITS bits, a monotone quantisation of
+// its preorder rank (code(x) > code(y) implies x > y), packed into a table 8x (4-bit) smaller
+// than FIRST that stays in L2.  Every slot looks up its target's code; the exact FIRST is
+// gathered only for the slots whose code equals the row's minimum or maximum code -- about two
+// per row plus a few percent of a hub row's slots.  The code boundaries are quantiles of
+// first[target] over a sample of slots (denser at both ends, where a long row's extremes
+// lie); they affect the number of exact gathers only, never the result.
+// The direction bits become conservative: code(target) >= code(row) looks the target up
+// (k_labels takes max(CID[row], CID[target]), which is right for every slot).
+// --------------------------------------------------------------------------
+#ifndef PG_TAG_BITS
+#define PG_TAG_BITS 4
+#endif
+constexpr int TAG_BITS = PG_TAG_BITS;
+constexpr int TAG_NB = (1 << TAG_BITS) - 1;           // boundaries; codes 0 .. TAG_NB
+constexpr int TAG_PW_SH = TAG_BITS == 4 ? 3 : 2;      // log2(codes per 32-bit word)
+constexpr int TAG_SAMPLES = 2048;
+static_assert(TAG_BITS == 4 || TAG_BITS == 8, "codes are nibbles or bytes");
+
+// sample position (of TAG_SAMPLES sorted values) of boundary j = 0 .. TAG_NB-1
+__device__ __forceinline__ int tag_bound_pos(int j) {
+    if (TAG_BITS == 8) return (j + 1) * (TAG_SAMPLES / 256);
+    // 4 bits: 1/64, 1/32, 1/16, 1/8, then steps of 3/32 up to 7/8, 15/16, 31/32, 63/64
+    const int U = TAG_SAMPLES / 64;
+    if (j < 4) return U << j;
+    if (j < 12) return 8 * U + 6 * U * (j - 3);
+    return TAG_SAMPLES - (U << (14 - j));
+}
+
+// one CTA: sample slots, sort first[target], pick the boundaries
+__global__ void __launch_bounds__(1024) k_tag_bounds(i64 m, const int32_t* __restrict__ tgt,
+                                                      const u32* __restrict__ FIRST, u32* BND) {
+    __shared__ u32 v[TAG_SAMPLES];
+    for (int i = threadIdx.x; i < TAG_SAMPLES; i += 1024) {
+        const u64 s = pg::sm64(0x7A65ull + (u64)i) % (u64)m;
+        v[i] = __ldg(FIRST + (u32)__ldg(tgt + s));
+    }
+    __syncthreads();
+    for (int k = 2; k <= TAG_SAMPLES; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < TAG_SAMPLES; i += 1024) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const u32 a = v[i], b = v[p];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        v[i] = b;
+                        v[p] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x < TAG_NB) BND[threadIdx.x] = v[tag_bound_pos(threadIdx.x)];
+}
+
+// code(f) = #{j : BND[j] <= f}, packed little-endian into Q
+__global__ void __launch_bounds__(256) k_tag_codes(i64 n, const u32* __restrict__ FIRST, const u32* __restrict__ BND,
+                                                    u32* __restrict__ Q) {
+    __shared__ u32 b[TAG_NB + 1];
+    for (int i = threadIdx.x; i < TAG_NB; i += 256) b[i] = BND[i];
+    if (threadIdx.x == 0) b[TAG_NB] = PG_INV;
+    __syncthreads();
+    constexpr int PW = 1 << TAG_PW_SH;
+    const i64 wi = (i64)blockIdx.x * 256 + threadIdx.x;
+    const i64 v0 = wi * PW;
+    if (v0 >= n) return;
+    u32 f[PW];
+    if (v0 + PW <= n) {
+#pragma unroll
+        for (int i = 0; i < PW; i += 4) {
+            const uint4 x = *reinterpret_cast<const uint4*>(FIRST + v0 + i);
+            f[i] = x.x, f[i + 1] = x.y, f[i + 2] = x.z, f[i + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PW; ++i) f[i] = v0 + i < n ? FIRST[v0 + i] : 0u;
+    }
+    u32 word = 0;
+#pragma unroll
+    for (int i = 0; i < PW; ++i) {
+        u32 c = 0;   // #{j : b[j] <= f}: binary search over the sorted boundaries
+#pragma unroll
+        for (int st = (TAG_NB + 1) >> 1; st >= 1; st >>= 1)
+            if (b[c + st - 1] <= f[i]) c += st;
+        word |= c << (TAG_BITS * i);
+    }
+    Q[wi] = word;
+}
+
+__device__ __forceinline__ u32 tag_code(u32 word, u32 v) {
+    return (word >> (TAG_BITS * (v & ((1u << TAG_PW_SH) - 1u)))) & (u32)TAG_NB;
+}
+// (min code, TAG_NB - max code) in the two halves of a word: one VIMNMX.U16x2 combines both
+__device__ __forceinline__ u32 tag_pair(u32 c) { return c | (((u32)TAG_NB - c) << 16); }
+
+#ifndef PG_TAGS2_MINB
+#define PG_TAGS2_MINB 5
+#endif
+#ifndef PG_TAGS2_QL1
+#define PG_TAGS2_QL1 0
+#endif
+__global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS2_MINB) k_tags2_blk(const i64* __restrict__ off,
+                                                                  const int32_t* __restrict__ tgt, i64 n, i64 m,
+                                                                  const u32* __restrict__ crow,
+                                                                  const u32* __restrict__ FIRST,
+                                                                  const u32* __restrict__ Q, uint2* W,
+                                                                  u32* __restrict__ DIR) {
+    __shared__ BlkSmem smem[WCH_BLOCK / 32];
+    const int lane = threadIdx.x & 31;
+    const i64 c = ((i64)blockIdx.x * WCH_BLOCK + threadIdx.x) >> 5;
+    if (c >= num_chunks(m)) return;
+    BlkSmem& sm = smem[threadIdx.x >> 5];
+    const i64 s0 = c * WCH, s1 = s0 + WCH < m ? s0 + WCH : m;
+    const i64 sl = s0 + BLK_SPL * lane;
+    const u32 base = crow[c];
+    const i64 a_base = off[base], e_base = off[(i64)base + 1];
+    const bool one_row = e_base >= s1;
+    constexpr u32 NEUT = 0xFFFFFFFFu;
+    u32 g[WCH_U], q[WCH_U];
+    wc_load(tgt, m, c, lane, g);
+    {
+        const u64 pol = policy_evict_last();   // the code table stays in L2 ahead of the streams
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k) {
+            q[k] = 0;
+            if (s0 + 32 * k + lane < s1)
+                q[k] = PG_TAGS2_QL1 ? ld_keep_l1(Q + (g[k] >> TAG_PW_SH), pol) : ld_keep(Q + (g[k] >> TAG_PW_SH), pol);
+        }
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k) q[k] = tag_code(q[k], g[k]);
+    }
+    if (one_row) {   // warp-uniform: a hub row's chunk
+        const u32 fb = __ldg(FIRST + base);
+        const u32 cb = tag_code(__ldg(Q + (base >> TAG_PW_SH)), base);
+        u32 x = NEUT;
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k)
+            if (s0 + 32 * k + lane < s1) x = __vminu2(x, tag_pair(q[k]));
+        u32 cmn = __reduce_min_sync(0xFFFFFFFFu, x & 0xFFFFu);
+        u32 cmx = (u32)TAG_NB - __reduce_min_sync(0xFFFFFFFFu, x >> 16);
+        // a minimum code above the row's own leaves w1 = first[row]; likewise the maximum
+        if (cmn > cb) cmn = NEUT;
+        if (cmx < cb) cmx = NEUT;
+        u32 cm = 0, dw = 0;
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k) {
+            const bool ok = s0 + 32 * k + lane < s1;
+            const bool cand = ok && (q[k] == cmn || q[k] == cmx);
+            if (cand) g[k] = ld_na(FIRST + g[k]);
+            cm |= (u32)cand << k;
+            const unsigned b = __ballot_sync(0xFFFFFFFFu, ok && q[k] >= cb);
+            if (lane == k) dw = b;
+        }
+        if (DIR && lane < WCH_U) DIR[(i64)WCH_U * c + lane] = dw;
+        u32 mn = PG_INV, mx = 0;
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k)
+            if (cm >> k & 1u) {
+                mn = g[k] < mn ? g[k] : mn;
+                mx = g[k] > mx ? g[k] : mx;
+            }
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        if (lane == 0 && mn != PG_INV) write_tag(W, fb, mn, mx, a_base < s0 || e_base > s1);
+        return;
+    }
+    u32 tb[BLK_SPL];
+    blk_transpose(sm, lane, g, tb);
+    uint2 cw;
+    {   // the codes take the same way, as bytes
+        __syncwarp();
+        uint8_t* cbuf = reinterpret_cast<uint8_t*>(sm.xp);
+#pragma unroll
+        for (int k = 0; k < WCH_U; ++k) cbuf[32 * k + lane] = (uint8_t)q[k];
+        __syncwarp();
+        cw = *reinterpret_cast<const uint2*>(cbuf + BLK_SPL * lane);
+    }
+    const BlkRows br = blk_rows(off, n, s0, s1, base, lane, sm);
+    const bool hstart = br.mb & 1u;
+    // (min, max) code of every row of the chunk, known to each of its slots: the lane's own
+    // pass, then a forward and a backward segmented scan over the lanes
+    u32 ci[BLK_SPL], fw[BLK_SPL];
+    u32 head = NEUT;
+    {
+        u32 acc = NEUT;
+        bool seen = false;
+#pragma unroll
+        for (int i = 0; i < BLK_SPL; ++i) {
+            ci[i] = ((i < 4 ? cw.x >> (8 * i) : cw.y >> (8 * (i - 4))) & 0xFFu);
+            if (br.mb >> i & 1u) {
+                if (!seen) head = acc;
+                seen = true;
+                acc = NEUT;
+            }
+            if (sl + i < s1) acc = __vminu2(acc, tag_pair(ci[i]));
+        }
+        if (!seen) head = acc;
+        fw[BLK_SPL - 1] = acc;   // the lane's last (open) row
+    }
+    const unsigned hb = __ballot_sync(0xFFFFFFFFu, br.mb != 0u);
+    u32 F = fw[BLK_SPL - 1], Bk = head;
+    {
+        const unsigned le = lane == 31 ? 0xFFFFFFFFu : (2u << lane) - 1u;
+        const int lo = (hb & le) ? 31 - __clz(hb & le) : 0;
+        const unsigned ge = hb >> lane;
+        const int hi = ge ? lane + __ffs(ge) - 1 : 31;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 a = __shfl_up_sync(0xFFFFFFFFu, F, o);
+            const u32 b = __shfl_down_sync(0xFFFFFFFFu, Bk, o);
+            if (lane - o >= lo) F = __vminu2(F, a);
+            if (lane + o <= hi) Bk = __vminu2(Bk, b);
+        }
+    }
+    u32 Fprev = __shfl_up_sync(0xFFFFFFFFu, F, 1), Bnext = __shfl_down_sync(0xFFFFFFFFu, Bk, 1);
+    if (lane == 0) Fprev = NEUT;
+    if (lane == 31) Bnext = NEUT;
+    {
+        u32 acc = Fprev;
+#pragma unroll
+        for (int i = 0; i < BLK_SPL; ++i) {
+            if (br.mb >> i & 1u) acc = NEUT;
+            if (sl + i < s1) acc = __vminu2(acc, tag_pair(ci[i]));
+            fw[i] = acc;
+        }
+    }
+    u32 cm = 0;
+    {
+        u32 full = __vminu2(fw[BLK_SPL - 1], Bnext);
+#pragma unroll
+        for (int i = BLK_SPL - 1; i >= 0; --i) {
+            if (i < BLK_SPL - 1 && (br.mb >> (i + 1) & 1u)) full = fw[i];
+            const bool cand = sl + i < s1 && (ci[i] == (full & 0xFFFFu) || (u32)TAG_NB - ci[i] == (full >> 16));
+            cm |= (u32)cand << i;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < BLK_SPL; ++i)
+        if (cm >> i & 1u) tb[i] = ld_na(FIRST + tb[i]);
+    // from here on as k_tags_blk, over the candidates only
+    const u32 fh = __ldg(FIRST + br.r_first);
+    u32 fr = fh;
+    u32 rc = tag_code(__ldg(Q + (br.r_first >> TAG_PW_SH)), br.r_first);
+    u32 mn = PG_INV, mx = 0, hmn = PG_INV, hmx = 0, db = 0;
+    bool in_head = true;
+#pragma unroll
+    for (int i = 0; i < BLK_SPL; ++i) {
+        if (i > 0 && (br.mb >> i & 1u)) {
+            if (in_head) {
+                hmn = mn;
+                hmx = mx;
+                in_head = false;
+                if (hstart) write_tag(W, fr, mn, mx, false);
+            } else {
+                write_tag(W, fr, mn, mx, false);
+            }
+            const u32 r = sm.row[BLK_SPL * lane + i];
+            fr = __ldg(FIRST + r);
+            rc = tag_code(__ldg(Q + (r >> TAG_PW_SH)), r);
+            mn = PG_INV;
+            mx = 0;
+        }
+        if (cm >> i & 1u) {
+            mn = tb[i] < mn ? tb[i] : mn;
+            mx = tb[i] > mx ? tb[i] : mx;
+        }
+        if (sl + i < s1) db |= (u32)(ci[i] >= rc) << i;
+    }
+    if (DIR) {
+        u32 x = db << (8 * (lane & 3));
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        if ((lane & 3) == 0) DIR[(i64)WCH_U * c + (lane >> 2)] = x;
+    }
+    const bool inner = (br.mb & 0xFEu) != 0;
+    u32 cmn = mn, cmx = mx;
+    bool started;
+    blk_seg_scan(lane, hstart || inner, cmn, cmx, started);
+    const u32 pmn = __shfl_up_sync(0xFFFFFFFFu, cmn, 1), pmx = __shfl_up_sync(0xFFFFFFFFu, cmx, 1);
+    const bool pstarted = __shfl_up_sync(0xFFFFFFFFu, (int)started, 1) != 0 && lane > 0;
+    if (inner && !hstart) {
+        const u32 tmn = lane > 0 && pmn < hmn ? pmn : hmn;
+        const u32 tmx = lane > 0 && pmx > hmx ? pmx : hmx;
+        write_tag(W, fh, tmn, tmx, !pstarted);
+    }
+    const bool next_starts = __shfl_down_sync(0xFFFFFFFFu, (int)hstart, 1) != 0;
+    if (lane < 31 && next_starts) write_tag(W, fr, cmn, cmx, !started);
+    if (lane == 31) write_tag(W, fr, cmn, cmx, !started || br.last_open);
+}
+
+// --------------------------------------------------------------------------
 // S4: low/high by a blocked sparse table over preorder positions (32-wide blocks)
 // --------------------------------------------------------------------------
 __device__ __forceinline__ uint2 mm(uint2 a, uint2 b) {
@@ -1792,7 +2087,10 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
 #pragma unroll
         for (int k = 0; k < H; ++k) {
             i64 s = s0 + 32 * (h + k) + lane;
-            const bool lk = s < s1 && ((__shfl_sync(0xFFFFFFFFu, dmask, h + k) >> lane) & 1u);
+            // every lane takes part in the shuffle (a short-circuited one leaves the source
+            // lane out in the last, partial window)
+            const u32 dwk = __shfl_sync(0xFFFFFFFFu, dmask, h + k);
+            const bool lk = s < s1 && ((dwk >> lane) & 1u);
             look |= (u32)lk << k;
             cw[k] = lk ? __ldg(GBIT + (w[h + k] >> 5)) : 0u;
         }
@@ -2122,6 +2420,15 @@ static bool dir_bits(i64 n, i64 m) {
     return (u64)cdiv(m, WCH) * WCH / 8 <= (u64)16 * (u64)(n > 0 ? n : 1);
 }
 
+// Two-level tags (code table + exact gathers of the extreme slots only): PASGAL_BCC_TAGS2=0/1
+// forces it.  The table (n * TAG_BITS / 8 bytes + 1 KB) lives in TA (8 bytes per vertex).
+static bool tags_two_level(i64 n, i64 m) {
+    const char* e = getenv("PASGAL_BCC_TAGS2");
+    if (m < 1) return false;
+    if (e) return e[0] != '0';
+    return false;
+}
+
 static unsigned vgc_grid() {
     static int blocks = 0;
     if (!blocks) {
@@ -2312,7 +2619,14 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // the Euler-tour array T (dead after the tour stage; room for up to 128 slots per vertex)
     u32* dir = out->edge_label && dir_bits(n, m) ? (u32*)w.T : nullptr;
     if (w.nch > 0) {
-        if (n >= ((i64)1 << 22))
+        if (tags_two_level(n, m)) {
+            // code table and its boundaries in the tour-arc array TA (8 bytes per vertex, dead)
+            u32* bnd = w.TA;
+            u32* Q = w.TA + 256;
+            PG_K(k_tag_bounds<<<1, 1024, 0, st>>>(m, tgt, w.FIRST, bnd));
+            PG_K(k_tag_codes<<<nblk(cdiv(n, (i64)1 << TAG_PW_SH), 256), 256, 0, st>>>(n, w.FIRST, bnd, Q));
+            PG_K(k_tags2_blk<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, Q, w.W, dir));
+        } else if (n >= ((i64)1 << 22))
             PG_K(k_tags_blk<true><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W, dir));
         else
             PG_K(k_tags_blk<false><<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, w.W, dir));
