@@ -106,6 +106,7 @@ struct Ws {
     u32* FPF;     // [position] parent's position | fence << 31 (PG_INV at roots)
     u32* C;       // Last-CC union-find over preorder positions
     u32* CIDV;    // per vertex: preorder rank of its skeleton component's head
+    u32* TQ;      // two-level tags: code boundaries (1 KB), then the packed code table
     u32* GBIT;    // per vertex bit: CIDV[v] == gcid (33 MB at 2^28: L2-resident)
     u32 *ROOTMARK, *UCNT, *UOFF, *CANON, *HEAVY;
     u32* CROW;
@@ -182,6 +183,7 @@ static size_t carve(Ws& w, char* base, i64 n, i64 m) {
     w.CANON = (u32*)take(4 * nn);
     w.HEAVY = (u32*)take(4 * nn);
     w.CROW = (u32*)take(4 * (w.nch + 1));
+    w.TQ = (u32*)take(1024 + 4 * cdiv(nn, 4));   // two-level tags: boundaries + code table (<= 1 byte per vertex)
     w.SCAN = (u64*)take(scan_status_bytes(scan_items > nn ? scan_items : nn));
     w.ctr = (Ctr*)take(sizeof(Ctr));
     return o + 256;
@@ -361,22 +363,24 @@ __device__ __forceinline__ void cc_sample_one(i64 v, int lb, const i64* __restri
 // C5a Last-CC 12.2 -> 11.4 ms; First-CC is slower above 4).
 constexpr int COMPRESS_ILP = 4, COMPRESS_ILP2 = 16;
 
+// Entries below `lo` are known self-roots and are neither read nor written (Last-CC: the
+// preorder slots [0, niso) of the isolated vertices, 63 % of the positions at C5a).
 template <int ILP>
-__device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i64 (&idx)[ILP]) {
+__device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i64 (&idx)[ILP], i64 lo = 0) {
     const i64 stride = (i64)gridDim.x * blockDim.x;
     const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     u32 x[ILP];
 #pragma unroll
     for (int j = 0; j < ILP; ++j) {
         idx[j] = t + j * stride;
-        x[j] = idx[j] < n ? ldcg(P + idx[j]) : 0u;
+        x[j] = idx[j] < n ? (idx[j] < lo ? (u32)idx[j] : ldcg(P + idx[j])) : 0u;
     }
     bool more = true;
     while (more) {
         more = false;
         u32 px[ILP];
 #pragma unroll
-        for (int j = 0; j < ILP; ++j) px[j] = idx[j] < n ? ldcg(P + x[j]) : x[j];
+        for (int j = 0; j < ILP; ++j) px[j] = idx[j] < n && idx[j] >= lo ? ldcg(P + x[j]) : x[j];
 #pragma unroll
         for (int j = 0; j < ILP; ++j) {
             if (px[j] != x[j]) {
@@ -388,7 +392,7 @@ __device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i6
 #pragma unroll
     for (int j = 0; j < ILP; ++j) {
         root[j] = x[j];
-        if (idx[j] < n) stcg(P + idx[j], x[j]);
+        if (idx[j] < n && idx[j] >= lo) stcg(P + idx[j], x[j]);
     }
 }
 
@@ -398,11 +402,12 @@ __device__ __forceinline__ void compress_ilp(i64 n, u32* P, u32 (&root)[ILP], i6
 #define PG_CMP_MINB 2
 #endif
 template <int ILP>
-__global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i64 n, u32* P, const u32* gate) {
+__global__ void __launch_bounds__(256, ILP >= 16 ? PG_CMP_MINB : 1) k_compress(i64 n, u32* P, const u32* gate,
+                                                                               const u32* lo = nullptr) {
     if (gated_off(gate, 0)) return;
     u32 root[ILP];
     i64 idx[ILP];
-    compress_ilp<ILP>(n, P, root, idx);
+    compress_ilp<ILP>(n, P, root, idx, lo ? (i64)*lo : 0);
 }
 
 // most frequent root among GIANT_SAMPLES seeded samples (ties -> smaller root).  Counts in
@@ -1011,11 +1016,9 @@ __global__ void __launch_bounds__(AC_B) k_arc_close(i64 n, uint2* HAB, const u32
     for (int i = 0; i < AC_V; ++i) {
         if (slot[i] == PG_INV) continue;
         const u32 v = (u32)(base + (i64)i * AC_B), f = s_base + slot[i];
+        // nothing reads the per-position records (PV, E, PPAR, W) of an isolated slot: every
+        // pass over positions starts at niso
         io.FL[v] = make_uint2(f, f);
-        io.PV[f] = v;
-        io.E[f] = f;
-        io.PPAR[f] = v;
-        io.W[f] = make_uint2(f, f);
     }
 }
 
@@ -1287,7 +1290,8 @@ __global__ void k_leaf_runs(const Ctr* ctr, const u32* __restrict__ bigp, const 
 // With leaf trimming it also places the leaves (LEAF map): leaf v of parent p with rank r
 // takes slot first[p] + 1 + r (E / PPAR / W of the slot were written by the parent).
 __global__ void k_vertex_first(i64 n, uint2* FL, const u32* __restrict__ PPAR, u32* FIRST, u32* out_parent,
-                               u32* out_first, const u32* __restrict__ LEAF, const uint2* __restrict__ LPR, u32* PV) {
+                               u32* out_first, const u32* __restrict__ LEAF, const uint2* __restrict__ LPR, u32* PV,
+                               const Ctr* ctr) {
     const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     u32 f;
@@ -1301,7 +1305,7 @@ __global__ void k_vertex_first(i64 n, uint2* FL, const u32* __restrict__ PPAR, u
     }
     FIRST[v] = f;
     if (out_first) out_first[v] = f;
-    if (out_parent) out_parent[v] = __ldg(PPAR + f);
+    if (out_parent) out_parent[v] = f < ctr->niso ? (u32)v : __ldg(PPAR + f);   // isolated: its own parent
 }
 
 // --------------------------------------------------------------------------
@@ -1740,10 +1744,15 @@ __device__ __forceinline__ uint2 shfl_idx2(uint2 v, int src) {
     return make_uint2(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src));
 }
 
-__global__ void k_rmq_block(i64 n, const uint2* __restrict__ W, uint2* PM, uint2* ST0) {
+// Positions [0, niso) are the isolated vertices' slots: no query range reaches them (a tree's
+// positions are contiguous and lie above), so their blocks are skipped and they enter the
+// boundary block as neutral elements.
+__global__ void k_rmq_block(i64 n, const uint2* __restrict__ W, uint2* PM, uint2* ST0, const Ctr* ctr) {
+    const i64 niso = ctr->niso;
+    if (((i64)blockIdx.x + 1) * blockDim.x <= niso) return;
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     int lane = threadIdx.x & 31;
-    uint2 v = i < n ? W[i] : make_uint2(PG_INV, 0u);
+    uint2 v = i < n && i >= niso ? W[i] : make_uint2(PG_INV, 0u);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         uint2 u = shfl_up2(v, o);
@@ -1753,9 +1762,9 @@ __global__ void k_rmq_block(i64 n, const uint2* __restrict__ W, uint2* PM, uint2
     if (lane == 31 && (i >> 5) < cdiv(n, 32)) ST0[i >> 5] = v;
 }
 
-__global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i64 half) {
+__global__ void k_rmq_level(i64 nb, const uint2* __restrict__ src, uint2* dst, i64 half, const Ctr* ctr) {
     i64 b = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
+    if (b >= nb || b < ((i64)ctr->niso >> 5) - 8) return;   // entries below the isolated slots' end are never read
     uint2 v = src[b];
     if (b + half < nb) v = mm(v, src[b + half]);
     dst[b] = v;
@@ -1782,12 +1791,17 @@ __global__ void __launch_bounds__(1024) k_rmq_levels_small(i64 nb, i64 lv, uint2
 __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __restrict__ E,
                             const u32* __restrict__ PV, const u32* __restrict__ PPAR,
                             const uint2* __restrict__ PM, const uint2* __restrict__ ST, i64 nb,
-                            const uint2* __restrict__ FL, u32* FPF, u32* C) {
+                            const uint2* __restrict__ FL, u32* FPF, const Ctr* ctr) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    const i64 niso = ctr->niso;
+    if (i - lane + 32 <= niso) {     // warp-uniform: isolated slots only (each its own root)
+        if (i < n) FPF[i] = PG_INV;
+        return;
+    }
     const bool valid = i < n;
-    uint2 w = valid ? W[i] : make_uint2(PG_INV, 0u);
-    u32 e = valid ? E[i] : (u32)i;
+    uint2 w = valid && i >= niso ? W[i] : make_uint2(PG_INV, 0u);
+    u32 e = valid && i >= niso ? E[i] : (u32)i;
     // in-register doubling table over [lane, lane + 2^k) within the 32-block
     uint2 M[6];
     M[0] = w;
@@ -1834,8 +1848,9 @@ __global__ void k_rmq_query(i64 n, const uint2* __restrict__ W, const u32* __res
             res = mm(res, mm(lvl[l], lvl[r - ((u64)1 << k) + 1]));
         }
     }
-    u32 v = PV[i], p = PPAR[i];
     u32 fpf = PG_INV;
+    u32 v = 0, p = 0;
+    if (i >= niso) v = PV[i], p = PPAR[i];
     if (p != v) {
         uint2 fp = FL[p];
         bool fence = fp.x <= res.x && res.y <= fp.y;
@@ -1861,13 +1876,20 @@ __device__ __forceinline__ bool is_cross(uint2 fu, uint2 fw) {
 // inside a block of LOCAL_B positions are joined in shared memory (a child's parent is
 // usually a few positions back), then C[i] = block root is published.
 __global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, int lb, const u32* __restrict__ FPF,
-                                                       const uint2* __restrict__ W, const u32* __restrict__ E, u32* C) {
+                                                       const uint2* __restrict__ W, const u32* __restrict__ E, u32* C,
+                                                       const Ctr* ctr) {
     __shared__ u32 sp[LOCAL_B];
     const i64 b0 = (i64)blockIdx.x << lb;
     const int cnt = (int)(n - b0 < (1 << lb) ? n - b0 : (1 << lb));
+    const i64 niso = ctr->niso;
+    if (b0 + cnt <= niso) {       // isolated slots only: singletons, nothing to read
+        for (int i = threadIdx.x; i < cnt; i += LOCAL_T) C[b0 + i] = (u32)(b0 + i);
+        return;
+    }
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) sp[i] = (u32)i;
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += LOCAL_T) {
+        if (b0 + i < niso) continue;
         u32 f = FPF[b0 + i];
         {     // the high tag's cross edge (k_cc2_links), when it stays in the block
             const u32 hi = __ldcs(&W[b0 + i].y);
@@ -1890,9 +1912,9 @@ __global__ void __launch_bounds__(LOCAL_T) k_cc2_local(i64 n, int lb, const u32*
 // the cross edge of its high tag (a cross edge never points into its own subtree, so
 // hi > last >= i and a block-local one was taken by k_cc2_local).
 __global__ void k_cc2_links(i64 n, int lb, const u32* __restrict__ FPF, const uint2* __restrict__ W,
-                            const u32* __restrict__ E, u32* C) {
+                            const u32* __restrict__ E, u32* C, const Ctr* ctr) {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || i < (i64)ctr->niso) return;
     const u32 f = FPF[i];
     const u32 hi = __ldcs(&W[i].y);
     const u32 e = __ldcs(E + i);
@@ -1908,7 +1930,7 @@ __global__ void k_cc2_rest(i64 n, const i64* __restrict__ off, const int32_t* __
                            const uint2* __restrict__ FL, const u32* __restrict__ PV, const u32* __restrict__ E,
                            const u32* __restrict__ P, u32* C, Ctr* ctr, u32* heavy) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || ldcg(C + i) == ctr->giant2) return;
+    if (i >= n || i < (i64)ctr->niso || ldcg(C + i) == ctr->giant2) return;
     u32 u = PV[i];
     if (P[u] == u) return;
     i64 a = off[u], b = off[u + 1];
@@ -1962,7 +1984,7 @@ __global__ void k_cc2_rest_heavy(i64 n, const i64* __restrict__ off, const int32
 __global__ void __launch_bounds__(256, PG_CMP_MINB) k_compress_final(i64 n, u32* C, Ctr* ctr) {
     u32 root[COMPRESS_ILP2];
     i64 idx[COMPRESS_ILP2];
-    compress_ilp<COMPRESS_ILP2>(n, C, root, idx);
+    compress_ilp<COMPRESS_ILP2>(n, C, root, idx, (i64)ctr->niso);
     u32 cnt = 0;
 #pragma unroll
     for (int j = 0; j < COMPRESS_ILP2; ++j) cnt += __popc(__ballot_sync(0xFFFFFFFFu, idx[j] < n && root[j] == (u32)idx[j]));
@@ -1982,12 +2004,14 @@ __global__ void __launch_bounds__(256, PG_CMP_MINB) k_compress_final(i64 n, u32*
 // the write-once ROOTMARK are read before any atomic -- a 33M-leaf star otherwise spent
 // 21 ms in same-address atomics on the hub.
 __global__ void k_artic(i64 n, const u32* __restrict__ PPAR, const u32* __restrict__ FPF, const u32* __restrict__ C,
-                        const u32* __restrict__ P, u32* ROOTMARK, u32* bits) {
+                        const u32* __restrict__ P, u32* ROOTMARK, u32* bits, const Ctr* ctr) {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 niso = ctr->niso;
+    if (((i64)blockIdx.x + 1) * blockDim.x <= (i64)niso) return;   // isolated slots: no tree edge
     const int lane = threadIdx.x & 31;
     bool head = false;
     u32 p = PG_INV, ci = 0;
-    if (i < n) {
+    if (i < n && i >= (i64)niso) {
         const u32 f = FPF[i];
         if (f != PG_INV && (f & 0x80000000u)) {
             ci = C[i];
@@ -2028,7 +2052,8 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
     if (v == 0) ctr->gcid = g;
     u32 cid = PG_INV;
     if (v < n) {
-        cid = __ldg(C + __ldg(FIRST + v));
+        const u32 f = __ldg(FIRST + v);
+        cid = f < ctr->niso ? f : __ldg(C + f);   // an isolated vertex is its own component
         CIDV[v] = cid;
         if (out_comp) out_comp[v] = cid;
     }
@@ -2045,6 +2070,9 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
 // only the remaining slots gather CIDV from HBM.
 #ifndef PG_LABELS_HALVES
 #define PG_LABELS_HALVES 8
+#endif
+#ifndef PG_LABELS_ONEROW
+#define PG_LABELS_ONEROW 8   // 0: off
 #endif
 __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
@@ -2067,9 +2095,44 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
     // the target (without DIR every slot does)
     u32 dmask = 0xFFFFFFFFu;
     if (DIR) dmask = __ldcs(DIR + (i64)WCH_U * c + (lane & (WCH_U - 1)));
+    u32 cur = crow[c];
+#if PG_LABELS_ONEROW
+    // One (hub) row over the whole chunk -- most slots of a power-law graph: no row search, and
+    // every window's lookups are in flight together: two dependent memory phases per chunk
+    // (bitmap, then the non-giant targets' CIDV) instead of two per window, which is what the
+    // kernel waits on
+    if (off[(i64)cur + 1] >= s1) {   // warp-uniform
+        const u32 cu = __ldg(CIDV + cur);
+        constexpr int OW = PG_LABELS_ONEROW;   // windows in flight together
+#pragma unroll
+        for (int h = 0; h < WCH_U; h += OW) {
+            u32 cw[OW];
+            u32 look = 0;
+#pragma unroll
+            for (int k = 0; k < OW; ++k) {
+                const u32 dwk = __shfl_sync(0xFFFFFFFFu, dmask, h + k);
+                const bool lk = s0 + 32 * (h + k) + lane < s1 && ((dwk >> lane) & 1u);
+                look |= (u32)lk << k;
+                cw[k] = lk ? __ldg(GBIT + (w[h + k] >> 5)) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < OW; ++k)
+                cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : ld_na(CIDV + w[h + k]);
+#pragma unroll
+            for (int k = 0; k < OW; ++k) {
+                const i64 s = s0 + 32 * (h + k) + lane;
+                if (s < s1) {
+                    u32 lab = cu > cw[k] ? cu : cw[k];
+                    if (w[h + k] == cur) lab = PG_INV;
+                    __stcs(label + s, lab);
+                }
+            }
+        }
+        return;
+    }
+#endif
     // the chunk in PG_LABELS_HALVES parts: fewer live registers (32 per thread, no spills)
     constexpr int H = WCH_U / PG_LABELS_HALVES;
-    u32 cur = crow[c];
 #pragma unroll
     for (int h = 0; h < WCH_U; h += H) {
         u32 cw[H], rw[H];
@@ -2421,12 +2484,16 @@ static bool dir_bits(i64 n, i64 m) {
 }
 
 // Two-level tags (code table + exact gathers of the extreme slots only): PASGAL_BCC_TAGS2=0/1
-// forces it.  The table (n * TAG_BITS / 8 bytes + 1 KB) lives in TA (8 bytes per vertex).
-static bool tags_two_level(i64 n, i64 m) {
+// forces it.
+static bool tags_two_level(i64 n, i64 m, const int32_t* tgt) {
     const char* e = getenv("PASGAL_BCC_TAGS2");
+    (void)tgt;
     if (m < 1) return false;
     if (e) return e[0] != '0';
-    return false;
+    // Its cost per slot does not depend on n (the code table stays in L2), k_tags_blk's grows
+    // with FIRST / L2: RMAT 2^26 5.7 vs 7.2 ms, 2^28 35.5 vs 27.8 ms.  Short rows (kNN, grids)
+    // gather two exact values per row anyway: C4 3.6 vs 4.9 ms.
+    return n >= ((i64)1 << 27) && m >= 8 * n;
 }
 
 static unsigned vgc_grid() {
@@ -2460,6 +2527,9 @@ static cudaError_t set_kernel_attributes() {
     // 90.7 ms at 100 %)
     if (PG_TAGS_CARVE >= 0)
         chk(cudaFuncSetAttribute(k_tags_blk<true>, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS_CARVE));
+#ifdef PG_TAGS2_CARVE
+    chk(cudaFuncSetAttribute(k_tags2_blk, cudaFuncAttributePreferredSharedMemoryCarveout, PG_TAGS2_CARVE));
+#endif
     chk(cudaFuncSetAttribute(k_wyllie_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(2 * sizeof(u32) * WY_MAX)));
     (void)vgc_grid();   // occupancy query cached outside any capture
@@ -2611,7 +2681,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
         PG_K(k_leaf_runs<<<HEAVY_GRID, 256, 0, st>>>(w.ctr, w.HEAVY, LCNT, w.FL, w.E, w.PPAR, w.W));
     }
     PG_K(k_vertex_first<<<nblk(n, B), B, 0, st>>>(n, w.FL, w.PPAR, w.FIRST, out->parent, out->first,
-                                                   trim ? fm.LEAF : nullptr, w.PM, w.PV));
+                                                   trim ? fm.LEAF : nullptr, w.PM, w.PV, w.ctr));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TOUR));
     // ---- S4 tags + RMQ (+ S5 tree-edge unions)
@@ -2619,10 +2689,9 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     // the Euler-tour array T (dead after the tour stage; room for up to 128 slots per vertex)
     u32* dir = out->edge_label && dir_bits(n, m) ? (u32*)w.T : nullptr;
     if (w.nch > 0) {
-        if (tags_two_level(n, m)) {
-            // code table and its boundaries in the tour-arc array TA (8 bytes per vertex, dead)
-            u32* bnd = w.TA;
-            u32* Q = w.TA + 256;
+        if (tags_two_level(n, m, tgt)) {
+            u32* bnd = w.TQ;
+            u32* Q = w.TQ + 256;
             PG_K(k_tag_bounds<<<1, 1024, 0, st>>>(m, tgt, w.FIRST, bnd));
             PG_K(k_tag_codes<<<nblk(cdiv(n, (i64)1 << TAG_PW_SH), 256), 256, 0, st>>>(n, w.FIRST, bnd, Q));
             PG_K(k_tags2_blk<<<chunk_blocks(m), WCH_BLOCK, 0, st>>>(off, tgt, n, m, w.CROW, w.FIRST, Q, w.W, dir));
@@ -2633,21 +2702,21 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     }
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_TAGS));
-    PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST));
+    PG_K(k_rmq_block<<<nblk(n, B), B, 0, st>>>(n, w.W, w.PM, w.ST, w.ctr));
     if (w.nb <= RMQ_SMALL) {
         if (w.lv > 1) PG_K(k_rmq_levels_small<<<1, 1024, 0, st>>>(w.nb, w.lv, w.ST));
     } else {
         for (i64 k = 1; k < w.lv; ++k)
             PG_K(k_rmq_level<<<nblk(w.nb, B), B, 0, st>>>(w.nb, w.ST + (k - 1) * w.nb, w.ST + k * w.nb,
-                                                          (i64)1 << (k - 1)));
+                                                          (i64)1 << (k - 1), w.ctr));
     }
-    PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FPF, w.C));
+    PG_K(k_rmq_query<<<nblk(n, B), B, 0, st>>>(n, w.W, w.E, w.PV, w.PPAR, w.PM, w.ST, w.nb, w.FL, w.FPF, w.ctr));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_RMQ));
     // ---- S5 Last-CC over cross edges
-    PG_K(k_cc2_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
-    PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C));
-    PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C, nullptr));
+    PG_K(k_cc2_local<<<(unsigned)cdiv(n, (i64)1 << lb), LOCAL_T, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C, w.ctr));
+    PG_K(k_cc2_links<<<nblk(n, B), B, 0, st>>>(n, lb, w.FPF, w.W, w.E, w.C, w.ctr));
+    PG_K(k_compress<COMPRESS_ILP2><<<nblk(cdiv(n, COMPRESS_ILP2), B), B, 0, st>>>(n, w.C, nullptr, &w.ctr->niso));
     PG_K(k_giant<<<1, GIANT_SAMPLES, 0, st>>>(n, w.C, seed + 0x9E3779B97F4A7C15ull, &w.ctr->giant2, nullptr));
     PG_K(k_cc2_rest<<<nblk(n, B), B, 0, st>>>(n, off, tgt, w.FL, w.PV, w.E, w.P, w.C, w.ctr, w.HEAVY));
     PG_K(k_cc2_rest_heavy<<<HEAVY_GRID, 256, 0, st>>>(n, off, tgt, w.FL, w.C, w.ctr, w.HEAVY));
@@ -2656,7 +2725,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_LAST_CC));
     // ---- S6 articulation, labels, count
-    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits));
+    PG_K(k_artic<<<nblk(n, B), B, 0, st>>>(n, w.PPAR, w.FPF, w.C, w.P, w.ROOTMARK, out->artic_bits, w.ctr));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_ARTIC));
     if (w.nch > 0 && out->edge_label)

@@ -24,8 +24,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--check", action="store_true", help="run checksum per set (canonical), must agree")
+    ap.add_argument("--scale", type=int, default=0, help="RMAT configs: scale override (draws scaled along)")
     a = ap.parse_args()
-    dg = pg.make_config(a.config)
+    dg = pg.make_config(a.config, scale_override=a.scale or None)
+    if a.scale:
+        a.config += f"@{a.scale}"
     torch.cuda.synchronize()
     n, m = dg.n, dg.m
     ws = torch.empty(pg.workspace_bytes(n, m), dtype=torch.uint8, device="cuda")
