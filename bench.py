@@ -413,9 +413,13 @@ def run_ours(args, rank, world, local):
     achieved = kb / (stage_ms[dom] / 1e3) / 1e9
     pipe_bytes = b_alg_pipeline(n, m)
     pipe_gbs = pipe_bytes / (statistics.mean(step_ms) / 1e3) / 1e9
-    traffic = traffic_from_profiles(args.config, KERNEL_NAMES[dom])
+    kname = KERNEL_NAMES[dom]
+    if dom == "tags" and _lib.load().pasgal_bcc_two_level_tags(n, m):
+        # two-level tags: the stage is k_tag_bounds + k_tag_codes (~1 % of it) + k_tags2_blk
+        kname = "k_tags2_blk"
+    traffic = traffic_from_profiles(args.config, kname)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": KERNEL_NAMES[dom],
+                "traffic": traffic, "kernel": kname,
                 "algorithmic_bytes_per_launch": kb, "kernel_ms": stage_ms[dom], "peak_source": peak_src,
                 "random_access": random_access_roofline(traffic, stage_ms[dom])}
     pipeline = {"algorithmic_bytes": pipe_bytes, "model": "56*M + 180*n (SURVEY 8(d))",

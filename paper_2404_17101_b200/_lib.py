@@ -54,6 +54,7 @@ _SZ = ctypes.c_size_t
 SIGNATURES = {
     "pasgal_bcc_workspace_bytes": (_SZ, [_I64, _I64]),
     "pasgal_csr_validate_workspace_bytes": (_SZ, [_I64, _I64]),
+    "pasgal_bcc_two_level_tags": (_INT, [_I64, _I64]),
     "pasgal_bcc": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP]),
     "pasgal_bcc_ex": (_INT, [ctypes.POINTER(PasgalCsr), ctypes.POINTER(PasgalBccOut), _VP, _SZ, _U64, _U32, _VP,
                              ctypes.POINTER(PasgalBccProf)]),

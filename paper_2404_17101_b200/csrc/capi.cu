@@ -6,6 +6,7 @@ namespace pg {
 int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws, size_t ws_bytes, u64 seed, u32 flags,
                cudaStream_t st, pasgal_bcc_prof_t* prof);
 size_t bcc_workspace_bytes(i64 n, i64 m);
+bool bcc_two_level_tags(i64 n, i64 m);
 size_t validate_workspace_bytes(i64 n, i64 m);
 int bits_to_bytes(const u32* bits, i64 n, uint8_t* out, cudaStream_t st);
 size_t adj_temp_bytes(i64 L);
@@ -65,6 +66,8 @@ size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots) {
     if (m_slots < 0) m_slots = 0;
     return pg::bcc_workspace_bytes(n, m_slots);
 }
+
+int pasgal_bcc_two_level_tags(int64_t n, int64_t m_slots) { return pg::bcc_two_level_tags(n, m_slots) ? 1 : 0; }
 
 static int check_bcc_args(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* workspace, uint32_t flags) {
     int s = check_csr(g);
