@@ -610,3 +610,38 @@ def test_degenerate_graphs_all_modes():
                 rr = pg.bcc_device(d_off, d_tgt, out=out, workspace=ws, graph=True)
                 assert int(rr.bcc_count.item()) == ref.bcc_count
     pg.release_workspace()
+
+
+def test_two_level_tags_forced(monkeypatch):
+    """The two-level tags kernel (default only from 2^27 vertices) forced on small and medium
+    graphs: KATs, the corpus, leafy forests, hub shapes with multi-chunk rows, and C2 --
+    canonical labels, articulation and count equal to the oracle, per-slot and vertex mode.
+    The library reports the forced choice through pasgal_bcc_two_level_tags."""
+    from paper_2404_17101_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.pasgal_bcc_two_level_tags(1 << 20, 1 << 24) == 0      # default: small graph
+    assert lib.pasgal_bcc_two_level_tags(1 << 28, 1 << 32) == 1      # default: C5a-sized
+    assert lib.pasgal_bcc_two_level_tags(1 << 28, 1 << 29) == 0      # default: sparse
+    monkeypatch.setenv("PASGAL_BCC_TAGS2", "1")
+    assert lib.pasgal_bcc_two_level_tags(1 << 10, 1 << 12) == 1
+    for case in golden_io.kats() + list(golden_io.corpus()):
+        check_case(case)
+    for name, off, tgt in _star_forest_cases():
+        ref = oracle.bcc_hopcroft_tarjan(off, tgt)
+        want = oracle.canonical_min_eid(off, tgt, ref.edge_label)
+        d_off = torch.from_numpy(off).cuda()
+        d_tgt = torch.from_numpy(tgt.view(np.int32)).cuda()
+        lab, art, cnt = _host_out(pg.bcc_device(d_off, d_tgt, canonical=True), off.shape[0] - 1)
+        assert cnt == ref.bcc_count, name
+        assert np.array_equal(art, ref.articulation.astype(bool)), name
+        assert np.array_equal(lab, want), name
+    # rows spanning many chunks next to short ones (one-row and blocked chunks, atomics at
+    # the chunk seams), and C2 (RMAT 2^20: 31.4 M slots)
+    n = 1 << 18
+    s = np.concatenate([np.zeros(n - 1, np.int64), np.arange(1, n - 1)])
+    t = np.concatenate([np.arange(1, n), np.arange(2, n)])
+    _parity_device_graph(pg.symmetrize_edges(n, s, t))
+    _parity_device_graph(pg.make_config("c2"))
+    monkeypatch.setenv("PASGAL_BCC_TAGS2", "0")
+    assert lib.pasgal_bcc_two_level_tags(1 << 28, 1 << 32) == 0

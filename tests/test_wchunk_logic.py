@@ -273,3 +273,138 @@ def test_validator_checker_rule_equals_oracle_is_symmetric():
     for trial in range(600):
         _, off, tgt = multigraph.perturbed(rng, trial)
         assert _validator_rule(off, tgt) == oracle.is_symmetric(off, tgt), trial
+
+
+# --------------------------------------------------------------------------
+# Two-level tags (k_tags2_blk): every slot carries a monotone 4-bit code of its value; the
+# exact value is used only where the code equals the row's minimum or maximum code.
+# --------------------------------------------------------------------------
+NEUT = 0xFFFFFFFF
+TAG_NB = 15
+
+
+def _vminu2(a, b):
+    return min(a & 0xFFFF, b & 0xFFFF) | (min(a >> 16, b >> 16) << 16)
+
+
+def _pair(c):
+    return c | ((TAG_NB - c) << 16)
+
+
+def tags2_candidates(mb, codes, nvalid):
+    """Lane-exact emulation of the candidate selection of k_tags2_blk's blocked path for one
+    chunk: the lane's own pass, the forward / backward segmented scans over the lanes
+    (Hillis-Steele steps with the segment bounds from one ballot), the second lane pass and
+    the backward sweep.  mb[lane] = start bits, codes[p] for p < nvalid.  Returns the set of
+    candidate positions."""
+    ci = [[codes[8 * l + i] if 8 * l + i < nvalid else 0 for i in range(8)] for l in range(32)]
+    val = [[8 * l + i < nvalid for i in range(8)] for l in range(32)]
+    head, tail = [], []
+    for l in range(32):
+        acc, seen, h = NEUT, False, NEUT
+        for i in range(8):
+            if (mb[l] >> i) & 1:
+                if not seen:
+                    h = acc
+                seen, acc = True, NEUT
+            if val[l][i]:
+                acc = _vminu2(acc, _pair(ci[l][i]))
+        if not seen:
+            h = acc
+        head.append(h)
+        tail.append(acc)
+    hb = sum(1 << l for l in range(32) if mb[l])
+    F, Bk = list(tail), list(head)
+    lo, hi = [], []
+    for l in range(32):
+        le = hb & ((2 << l) - 1)
+        lo.append(le.bit_length() - 1 if le else 0)
+        ge = hb >> l
+        hi.append(l + ((ge & -ge).bit_length() - 1) if ge else 31)
+    o = 1
+    while o < 32:
+        Fn, Bn = list(F), list(Bk)
+        for l in range(32):
+            if l - o >= lo[l]:
+                Fn[l] = _vminu2(F[l], F[l - o])
+            if l + o <= hi[l]:
+                Bn[l] = _vminu2(Bk[l], Bk[l + o])
+        F, Bk = Fn, Bn
+        o <<= 1
+    cand = set()
+    for l in range(32):
+        fprev = F[l - 1] if l > 0 else NEUT
+        bnext = Bk[l + 1] if l < 31 else NEUT
+        fw, acc = [], fprev
+        for i in range(8):
+            if (mb[l] >> i) & 1:
+                acc = NEUT
+            if val[l][i]:
+                acc = _vminu2(acc, _pair(ci[l][i]))
+            fw.append(acc)
+        full = _vminu2(fw[7], bnext)
+        for i in range(7, -1, -1):
+            if i < 7 and (mb[l] >> (i + 1)) & 1:
+                full = fw[i]
+            if val[l][i] and (ci[l][i] == (full & 0xFFFF) or TAG_NB - ci[l][i] == (full >> 16)):
+                cand.add(8 * l + i)
+    return cand
+
+
+def emulate_tags2(off, vals, first, bounds):
+    """k_tags2_blk: W (min, max) per row from the exact values of the candidate slots only."""
+    n = off.shape[0] - 1
+    m = int(off[-1])
+    code = lambda x: int(np.searchsorted(bounds, x, side="right"))
+    W = [[int(first[r]), int(first[r])] for r in range(n)]
+    ncand = 0
+    for c in range((m + WCH - 1) // WCH):
+        s0, s1 = c * WCH, min(c * WCH + WCH, m)
+        base = chunk_row(off, n, s0)
+        codes = [code(int(vals[s])) for s in range(s0, s1)]
+        if int(off[base + 1]) >= s1:        # one row over the whole chunk
+            cb = code(int(first[base]))
+            cmn, cmx = min(codes), max(codes)
+            cmn = None if cmn > cb else cmn
+            cmx = None if cmx < cb else cmx
+            cand = [s for s in range(s0, s1) if codes[s - s0] in (cmn, cmx)]
+            rows = {s: base for s in cand}
+        else:
+            mb, rfirst, rowat, _ = blk_rows(off, n, s0, s1, base)
+            cset = tags2_candidates(mb, codes, s1 - s0)
+            # candidates = exactly the slots at the extreme codes of their row within the chunk
+            rowof, r = [], base
+            for p in range(s1 - s0):
+                r = rowat.get(p, r)
+                rowof.append(r)
+            for rr in set(rowof):
+                ps = [p for p in range(s1 - s0) if rowof[p] == rr]
+                lo, hi = min(codes[p] for p in ps), max(codes[p] for p in ps)
+                assert {p for p in ps if p in cset} == {p for p in ps if codes[p] in (lo, hi)}, (c, rr)
+            cand = [s0 + p for p in sorted(cset)]
+            rows = {s0 + p: rowof[p] for p in cset}
+        ncand += len(cand)
+        for s in cand:
+            r = rows[s]
+            W[r][0] = min(W[r][0], int(vals[s]))
+            W[r][1] = max(W[r][1], int(vals[s]))
+    return W, ncand
+
+
+def test_tags2_candidates_give_exact_tags():
+    """For any monotone code, the candidate slots alone reproduce every row's min / max, and
+    the candidate set is exactly the slots at their row's extreme codes (per chunk)."""
+    rng = np.random.default_rng(11)
+    for trial, n, off, vals, first in _random_csrs(9, 40):
+        hi = 10 * n
+        kinds = [np.sort(rng.integers(0, hi, TAG_NB)),                 # arbitrary boundaries
+                 np.full(TAG_NB, hi + 1),                               # one code for everything
+                 np.quantile(vals, np.linspace(0, 1, TAG_NB + 2)[1:-1]).astype(np.int64)]
+        bounds = kinds[trial % 3]
+        W, ncand = emulate_tags2(off, vals, first, bounds)
+        for r in range(n):
+            seg = vals[off[r]:off[r + 1]]
+            want = [int(first[r]), int(first[r])] if seg.shape[0] == 0 else \
+                [min(int(first[r]), int(seg.min())), max(int(first[r]), int(seg.max()))]
+            assert W[r] == want, (trial, r)
+        assert ncand <= int(off[-1])
