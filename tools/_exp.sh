@@ -1,4 +1,3 @@
-ncu --set full --import-source on --clock-control none -k regex:"k_tags2_blk" -c 1 -o gpurun_out/full_t2 python tools/profile_run.py --config c5a --calls 1 > gpurun_out/ncu_full_t2.log 2>&1
-ncu -i gpurun_out/full_t2.ncu-rep --page source --csv > gpurun_out/full_t2v1_source.csv 2>&1
-ncu -i gpurun_out/full_t2.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/full_t2v1_source_cuda.csv 2>&1
-rm -f gpurun_out/full_t2.ncu-rep
+python -m pytest tests/test_gpu_parity.py -x -q -k "kats or corpus or singles or hub or degenerate or leaf or two_level or c2 or c3" > gpurun_out/cmp_tests.log 2>&1; echo "exit $?" >> gpurun_out/cmp_tests.log
+python tools/env_sweep.py --config c5a --check --rounds 2 --sets "A=1" > gpurun_out/exp6.out 2>&1
+python tools/config_times.py c2 c3 c4 >> gpurun_out/exp6.out 2>&1
