@@ -1539,6 +1539,9 @@ __device__ __forceinline__ u32 tag_pair(u32 c) { return c | (((u32)TAG_NB - c) <
 #ifndef PG_TAGS2_QL1
 #define PG_TAGS2_QL1 0
 #endif
+#ifndef PG_TAGS2_EXACT
+#define PG_TAGS2_EXACT ld_na64
+#endif
 __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS2_MINB) k_tags2_blk(const i64* __restrict__ off,
                                                                   const int32_t* __restrict__ tgt, i64 n, i64 m,
                                                                   const u32* __restrict__ crow,
@@ -1586,7 +1589,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS2_MINB) k_tags2_blk(const i6
         for (int k = 0; k < WCH_U; ++k) {
             const bool ok = s0 + 32 * k + lane < s1;
             const bool cand = ok && (q[k] == cmn || q[k] == cmx);
-            if (cand) g[k] = ld_na(FIRST + g[k]);
+            if (cand) g[k] = PG_TAGS2_EXACT(FIRST + g[k]);
             cm |= (u32)cand << k;
             const unsigned b = __ballot_sync(0xFFFFFFFFu, ok && q[k] >= cb);
             if (lane == k) dw = b;
@@ -1676,7 +1679,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_TAGS2_MINB) k_tags2_blk(const i6
     }
 #pragma unroll
     for (int i = 0; i < BLK_SPL; ++i)
-        if (cm >> i & 1u) tb[i] = ld_na(FIRST + tb[i]);
+        if (cm >> i & 1u) tb[i] = PG_TAGS2_EXACT(FIRST + tb[i]);
     // from here on as k_tags_blk, over the candidates only
     const u32 fh = __ldg(FIRST + br.r_first);
     u32 fr = fh;
@@ -2074,6 +2077,9 @@ __global__ void k_cid_vertices(i64 n, const u32* __restrict__ C, const u32* __re
 #ifndef PG_LABELS_ONEROW
 #define PG_LABELS_ONEROW 4   // windows in flight together; 0: off (C5a labels 16.1 -> 14.9 ms; 8: 15.6)
 #endif
+#ifndef PG_LABELS_GATHER
+#define PG_LABELS_GATHER ld_na64
+#endif
 __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64* __restrict__ off, const int32_t* __restrict__ tgt,
                                                       i64 n, i64 m, const u32* __restrict__ crow,
                                                       const u32* __restrict__ CIDV, const u32* __restrict__ GBIT,
@@ -2117,7 +2123,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
             }
 #pragma unroll
             for (int k = 0; k < OW; ++k)
-                cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : ld_na(CIDV + w[h + k]);
+                cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : PG_LABELS_GATHER(CIDV + w[h + k]);
 #pragma unroll
             for (int k = 0; k < OW; ++k) {
                 const i64 s = s0 + 32 * (h + k) + lane;
@@ -2159,7 +2165,7 @@ __global__ void __launch_bounds__(WCH_BLOCK, PG_LABELS_MINB) k_labels(const i64*
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : ld_na(CIDV + w[h + k]);
+            cw[k] = !(look >> k & 1u) ? 0u : (cw[k] >> (w[h + k] & 31)) & 1u ? g : PG_LABELS_GATHER(CIDV + w[h + k]);
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {

@@ -52,6 +52,13 @@ __device__ __forceinline__ u32 ld_na(const u32* p) {
     asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
+// the same with the smallest L2 fetch hint: an isolated 4-byte gather otherwise brings a
+// whole 128-byte line from DRAM (section 4.3 of DESIGN.md)
+__device__ __forceinline__ u32 ld_na64(const u32* p) {
+    u32 r;
+    asm("ld.global.nc.L1::no_allocate.L2::64B.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ void stcg(u32* p, u32 v) { __stcg(p, v); }
 
 __device__ __forceinline__ u64 ld_volatile_u64(const u64* p) {
