@@ -158,7 +158,7 @@ int pasgal_csr_validate_check(const pasgal_csr_t* g, void* workspace, size_t wor
 /* Workspace for pasgal_csr_validate: 4 bytes per slot (one bucketed 8-byte key per run of
  * "up" slots, at most m/2 of them) plus ~8 KB per CTA of histograms -- O(m), like the
  * reference's twin array (oracles.py:107-116).  This is NOT the size pasgal_bcc needs
- * (pasgal_bcc_workspace_bytes is O(n), ~143 B per vertex): graphs with more than ~36 slots
+ * (pasgal_bcc_workspace_bytes is O(n), ~144 B per vertex): graphs with more than ~36 slots
  * per vertex need more here.  One buffer may serve both calls when they run one after the
  * other on one stream (pasgal_csr_validate has returned before pasgal_bcc is called) if it
  * holds max(pasgal_bcc_workspace_bytes, pasgal_csr_validate_workspace_bytes) bytes. */

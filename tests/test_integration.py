@@ -5,7 +5,7 @@ from INTEGRATION.md -- so the documented code is the tested code -- with only it
 import of BccLabels pointed at this package's identical container (results.py:45-88), and
 run on reference-shaped graphs: a `Graph` with `n`, `m`, int64 `offsets` and uint32 or
 int64 `targets` (graph.py:54-129).  The dense case (M/n > 64) is the one a workspace-size
-mistake breaks: validation needs 4 B per slot, FAST-BCC ~143 B per vertex.
+mistake breaks: validation needs 4 B per slot, FAST-BCC ~144 B per vertex.
 """
 
 import ctypes
