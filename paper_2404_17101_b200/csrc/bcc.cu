@@ -2499,7 +2499,16 @@ static bool tags_two_level(i64 n, i64 m, const int32_t* tgt) {
     // Its cost per slot does not depend on n (the code table stays in L2), k_tags_blk's grows
     // with FIRST / L2: RMAT 2^26 5.7 vs 7.2 ms, 2^28 35.5 vs 27.8 ms.  Short rows (kNN, grids)
     // gather two exact values per row anyway: C4 3.6 vs 4.9 ms.
-    return n >= ((i64)1 << 27) && m >= 8 * n;
+    // "from 2^27 vertices" on a B200: FIRST (4 bytes per vertex) at least 4x the L2
+    static i64 l2 = 0;
+    if (!l2) {
+        int dev = 0, bytes = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess || bytes <= 0)
+            bytes = 126 << 20;
+        l2 = bytes;
+    }
+    return n >= l2 && m >= 8 * n;
 }
 
 static unsigned vgc_grid() {
