@@ -81,8 +81,9 @@ size_t pasgal_bcc_workspace_bytes(int64_t n, int64_t m_slots);
 
 /* 1 when pasgal_bcc computes the S4 tags of a graph of this size with the two-level kernel
  * (a 4-bit code table kept in L2, exact preorder ranks gathered only for a row's extreme
- * slots) instead of one rank gather per slot: from 2^27 vertices and 8 slots per vertex on,
- * or as PASGAL_BCC_TAGS2=0/1 forces.  Reporting only (bench.py names the kernel it timed);
+ * slots) instead of one rank gather per slot: once the rank array (4 bytes per vertex) is
+ * at least 4x the device's L2 (2^27 vertices on a B200) and the graph has 8 slots per
+ * vertex, or as PASGAL_BCC_TAGS2=0/1 forces.  Reporting only (bench.py names the kernel it timed);
  * results are identical either way. */
 int pasgal_bcc_two_level_tags(int64_t n, int64_t m_slots);
 
