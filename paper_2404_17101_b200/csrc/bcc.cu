@@ -924,15 +924,14 @@ __global__ void k_forest_marks(i64 n, const uint2* __restrict__ HAB, ForestMarks
 
 
 // Close every out-arc list into a cycle (a root's cycle exits through its up arc).  Roots:
-//   isolated (no forest arc): preorder slot f from a warp-aggregated counter, written here;
+//   isolated (no forest arc): preorder slot f from a warp-aggregated counter; only FL[v] is
+//   written (no pass over positions reads the records of a slot below niso);
 //   otherwise succ(2r) = NEXT[2r+1] = first out-arc of r, and succ(2r+1) = NEXT[2r] = the
 //   down arc of the root chained before r (warp-aggregated atomicExch on ctr->roothead).
 // Neither the order of trees on the tour nor the order of isolated slots matters.
 
 struct IsoOut {
     uint2* FL;
-    u32 *PV, *E, *PPAR;
-    uint2* W;
     u32* ROOTMARK;
 };
 
@@ -2664,7 +2663,7 @@ int bcc_launch(const pasgal_csr_t* g, const pasgal_bcc_out_t* out, void* ws_ptr,
     PG_K(k_arc_link_blk<<<nblk(n, AL_T), AL_T, 0, st>>>(n, w.HAB, w.HEAD, w.NEXT, !trim, fm, LCNT, w.PM, w.ctr));
     PG_K(k_arc_close<<<nblk(n, AC_B * AC_V), AC_B, 0, st>>>(
         n, w.HAB, w.HEAD, w.P, fm, w.ctr, w.NEXT,
-        IsoOut{w.FL, w.PV, w.E, w.PPAR, w.W, w.ROOTMARK}));
+        IsoOut{w.FL, w.ROOTMARK}));
     PG_LAUNCH_CHECK();
     PG_CUDA_TRY(mark(PASGAL_STAGE_FOREST));
     // ---- S3 list ranking
