@@ -620,6 +620,7 @@ def test_two_level_tags_forced(monkeypatch):
     from paper_2404_17101_b200 import _lib
 
     lib = _lib.load()
+    monkeypatch.delenv("PASGAL_BCC_TAGS2", raising=False)            # (the suite may run with it forced)
     assert lib.pasgal_bcc_two_level_tags(1 << 20, 1 << 24) == 0      # default: small graph
     assert lib.pasgal_bcc_two_level_tags(1 << 28, 1 << 32) == 1      # default: C5a-sized
     assert lib.pasgal_bcc_two_level_tags(1 << 28, 1 << 29) == 0      # default: sparse
